@@ -1,0 +1,435 @@
+// fs_gram_tc.cu — pairwise mask-overlap (Gram) matrix on 5th-gen tensor cores.
+//
+// Reference: similarity_matrix() issues one pair_counts() per i<j pair
+// (analytics.py:174-181, _kernels_np.py:26-32): |A & B| over wet masks.  Stacking the
+// binarized masks as X (k x P, 0/1) gives I = X X^T, a dense contraction over pixels.
+//
+// Engine: tcgen05.mma.cta_group::1.kind::i8 (u8 x u8 -> s32 in TMEM).
+//  * Masks stay bit-packed in HBM (P/8 bytes each).  Producer warps load 16 B (128 px)
+//    per mask row per stage and expand bits to 0/1 bytes directly into the canonical
+//    K-major SWIZZLE_128B shared-memory layout (one 128-B swizzle row per mask).
+//  * Masks are tiled in panels of PANEL (128 or 256) rows.  A diagonal tile (I == I)
+//    uses ONE smem panel as both the A and the B operand, so every mask row is
+//    expanded once per K step; the MMA reads it as M rows and as N columns.
+//  * PANEL = 256: two M=128 halves.  Diagonal tiles issue half 0 with N=256 and half 1
+//    with N=128 (columns 128..255) — the lower-left quadrant is the transpose of the
+//    upper-right one and is mirrored by the reduce kernel (3/4 of the full work).
+//  * Pixels (K) are split over CTAs; each CTA writes an int32 partial tile and a reduce
+//    kernel sums partials into the exact int64 Gram.  Partials are exact: a CTA's K
+//    range is far below 2^31 pixels.
+#include <cstdio>
+
+#include "fs_internal.h"
+
+namespace fs {
+
+namespace tc {
+
+constexpr int kThreads = 160;  // warp 0: TMEM alloc + MMA issue; warps 1..4: producers/epilogue
+constexpr int kStagePx = 128;  // K per stage: one 128-B SW128 row per mask
+constexpr int kSmemBudget = 200 * 1024;
+constexpr int kPrefetch = 4;   // producer register prefetch depth (stages)
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);   // start address
+  d |= (uint64_t)1u << 16;                       // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;             // SBO: 8 rows x 128 B
+  d |= (uint64_t)1u << 46;                       // descriptor version (sm_100)
+  d |= (uint64_t)2u << 61;                       // SWIZZLE_128B
+  return d;
+}
+
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4)                       // D format: S32
+         | (0u << 7) | (0u << 10)        // A, B: unsigned 8-bit
+         | ((uint32_t)(N >> 3) << 17)    // N
+         | ((uint32_t)(M >> 4) << 24);   // M
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   ptx::smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 16 bits -> 16 bytes of 0/1, written as one swizzled 16-B chunk
+__device__ __forceinline__ uint4 expand16(uint32_t half) {
+  uint4 o;
+  o.x = ((half & 0xFu) * 0x00204081u) & 0x01010101u;
+  o.y = (((half >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
+  o.z = (((half >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
+  o.w = (((half >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
+  return o;
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Expand one 128-px row (4 words) into the SW128 row `row` of a panel at `base`.
+__device__ __forceinline__ void expand_row(uint32_t base, uint32_t row, uint4 v) {
+  const uint32_t rbase = base + row * 128u;
+  const uint32_t sw = row & 7u;
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint32_t half = (w[c >> 1] >> ((c & 1) * 16)) & 0xFFFFu;
+    st_shared_v4(rbase + (((uint32_t)c ^ sw) << 4), expand16(half));
+  }
+}
+
+template <int PANEL, bool DIAG>
+struct Cfg {
+  static constexpr int kRowsPerThread = PANEL / 128;        // per region
+  static constexpr int kRegions = DIAG ? 1 : 2;
+  static constexpr int kRegionBytes = PANEL * 128;
+  static constexpr int kStageBytes = kRegionBytes * kRegions;
+  static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
+  static constexpr int kHalves = PANEL / 128;
+  static constexpr uint32_t kTmemCols = PANEL == 256 ? 512u : 128u;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int PANEL, bool DIAG>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gram_tc(const uint32_t *__restrict__ packed, uint64_t wpm, const uint32_t *__restrict__ slots,
+              uint32_t k, uint32_t npanels, uint32_t kchunks, uint64_t stages_per_chunk,
+              uint64_t total_stages, int32_t *__restrict__ partial) {
+  using C = Cfg<PANEL, DIAG>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+  const uint32_t pad = (1024u - (raw_addr & 1023u)) & 1023u;
+  uint8_t *smem = smem_raw + pad;
+  const uint32_t smem_base = raw_addr + pad;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);
+  uint64_t *empty = full + C::kStages;
+  uint64_t *tmem_full = empty + C::kStages;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  // tile decode: blockIdx.x = tile * kchunks + kc
+  const uint32_t tile = blockIdx.x / kchunks;
+  const uint32_t kc = blockIdx.x % kchunks;
+  uint32_t I, J;
+  if (DIAG) {
+    I = J = tile;
+  } else {
+    uint32_t t = tile;
+    I = 0;
+    while (t >= npanels - 1 - I) {
+      t -= npanels - 1 - I;
+      ++I;
+    }
+    J = I + 1 + t;
+  }
+  const uint64_t st0 = (uint64_t)kc * stages_per_chunk;
+  const uint64_t st1 = min(st0 + stages_per_chunk, total_stages);
+  const int nst = st1 > st0 ? (int)(st1 - st0) : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&full[s], 128);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(tmem_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     ptx::smem_u32(tmem_slot)),
+                 "n"(C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== MMA issuer =====
+    if (lane == 0 && nst > 0) {
+      constexpr uint32_t idA = idesc_i8(128, PANEL);
+      constexpr uint32_t idB = idesc_i8(128, 128);
+      for (int j = 0; j < nst; ++j) {
+        const int s = j % C::kStages;
+        ptx::mbar_wait(&full[s], (uint32_t)((j / C::kStages) & 1));
+        fence_after();
+        const uint32_t a_base = smem_base + s * C::kStageBytes;
+        const uint32_t b_base = DIAG ? a_base : a_base + C::kRegionBytes;
+#pragma unroll
+        for (int ks = 0; ks < kStagePx / 32; ++ks) {
+          const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
+#pragma unroll
+          for (int h = 0; h < C::kHalves; ++h) {
+            const uint64_t adesc = sw128_desc(a_base + h * 128 * 128 + ks * 32);
+            if (DIAG && PANEL == 256 && h == 1) {
+              // rows 128..255 x cols 128..255 only
+              const uint64_t bdesc = sw128_desc(b_base + 128 * 128 + ks * 32);
+              mma_i8(tmem + 256u, adesc, bdesc, idB, acc);
+            } else {
+              const uint64_t bdesc = sw128_desc(b_base + ks * 32);
+              mma_i8(tmem + (uint32_t)(h * PANEL), adesc, bdesc, idA, acc);
+            }
+          }
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    // ===== producers: bits -> 0/1 bytes in SW128 K-major smem =====
+    const uint32_t ptid = (uint32_t)(tid - 32);
+    const uint32_t *rowp[C::kRegions][C::kRowsPerThread];
+#pragma unroll
+    for (int r = 0; r < C::kRegions; ++r)
+#pragma unroll
+      for (int m = 0; m < C::kRowsPerThread; ++m) {
+        const uint32_t panel = (r == 0) ? I : J;
+        const uint32_t row = panel * PANEL + ptid + m * 128;
+        rowp[r][m] = row < k ? packed + (uint64_t)__ldg(slots + row) * wpm : nullptr;
+      }
+    uint4 buf[kPrefetch][C::kRegions][C::kRowsPerThread];
+    auto load_stage = [&](int j, uint4 (&dst)[C::kRegions][C::kRowsPerThread]) {
+#pragma unroll
+      for (int r = 0; r < C::kRegions; ++r)
+#pragma unroll
+        for (int m = 0; m < C::kRowsPerThread; ++m) {
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (j < nst && rowp[r][m] != nullptr)
+            v = ptx::ld_nc_v4(rowp[r][m] + (st0 + (uint64_t)j) * (kStagePx / 32));
+          dst[r][m] = v;
+        }
+    };
+#pragma unroll
+    for (int d = 0; d < kPrefetch; ++d) load_stage(d, buf[d]);
+    for (int j0 = 0; j0 < nst; j0 += kPrefetch) {
+#pragma unroll
+      for (int d = 0; d < kPrefetch; ++d) {
+        const int j = j0 + d;
+        if (j < nst) {
+          const int s = j % C::kStages;
+          if (j >= C::kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / C::kStages) - 1) & 1));
+          const uint32_t sbase = smem_base + s * C::kStageBytes;
+#pragma unroll
+          for (int r = 0; r < C::kRegions; ++r)
+#pragma unroll
+            for (int m = 0; m < C::kRowsPerThread; ++m)
+              expand_row(sbase + r * C::kRegionBytes, ptid + m * 128, buf[d][r][m]);
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&full[s]);
+          load_stage(j + kPrefetch, buf[d]);
+        }
+      }
+    }
+    // ===== epilogue: TMEM -> registers -> int32 partial tile =====
+    const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp
+    int32_t *out = partial + (uint64_t)blockIdx.x * PANEL * PANEL;
+    if (nst > 0) {
+      ptx::mbar_wait(tmem_full, 0);
+      fence_after();
+    }
+#pragma unroll
+    for (int h = 0; h < C::kHalves; ++h) {
+      const uint32_t row = h * 128 + q * 32 + lane;
+      const bool lower_diag = DIAG && PANEL == 256 && h == 1;
+      const int c_begin = lower_diag ? 128 : 0;
+      for (int c0 = c_begin; c0 < PANEL; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t col = lower_diag ? (256u + (uint32_t)(c0 - 128)) : (uint32_t)(h * PANEL + c0);
+        tmem_ld32(tmem + ((q * 32u) << 16) + col, v);
+        if (nst == 0) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = 0;
+        }
+        int4 *dst = reinterpret_cast<int4 *>(out + (uint64_t)row * PANEL + c0);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          dst[e] = make_int4((int)v[4 * e], (int)v[4 * e + 1], (int)v[4 * e + 2], (int)v[4 * e + 3]);
+      }
+    }
+    fence_before();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(C::kTmemCols));
+  }
+}
+
+// Sum int32 partials over K chunks; scatter into the k x k Gram (both triangles).
+template <int PANEL>
+__global__ void k_gram_reduce(const int32_t *__restrict__ part_diag, uint32_t kc_diag,
+                              const int32_t *__restrict__ part_off, uint32_t kc_off, uint32_t k,
+                              uint32_t npanels, unsigned long long *__restrict__ gram) {
+  const uint32_t ndiag = npanels;
+  const uint32_t noff = npanels * (npanels - 1) / 2;
+  const uint64_t per_tile = (uint64_t)PANEL * PANEL;
+  const uint64_t total = (uint64_t)(ndiag + noff) * per_tile;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(e / per_tile);
+    const uint32_t r = (uint32_t)((e % per_tile) / PANEL), c = (uint32_t)(e % PANEL);
+    uint32_t I, J;
+    const int32_t *base;
+    uint32_t kc;
+    uint32_t rr = r, cc = c;
+    if (t < ndiag) {
+      I = J = t;
+      base = part_diag + (uint64_t)t * kc_diag * per_tile;
+      kc = kc_diag;
+      if (PANEL == 256 && r >= 128 && c < 128) {  // not computed: mirror quadrant
+        rr = c;
+        cc = r;
+      }
+    } else {
+      uint32_t u = t - ndiag;
+      I = 0;
+      while (u >= npanels - 1 - I) {
+        u -= npanels - 1 - I;
+        ++I;
+      }
+      J = I + 1 + u;
+      base = part_off + (uint64_t)(t - ndiag) * kc_off * per_tile;
+      kc = kc_off;
+    }
+    const uint32_t gi = I * PANEL + r, gj = J * PANEL + c;
+    if (gi >= k || gj >= k) continue;
+    long long s = 0;
+    for (uint32_t x = 0; x < kc; ++x) s += base[(uint64_t)x * per_tile + (uint64_t)rr * PANEL + cc];
+    gram[(uint64_t)gi * k + gj] = (unsigned long long)s;
+    if (I != J) gram[(uint64_t)gj * k + gi] = (unsigned long long)s;
+  }
+}
+
+struct Plan {
+  int panel;
+  uint32_t npanels, ndiag, noff;
+  uint64_t total_stages;
+  uint32_t kc_diag, kc_off;
+  uint64_t spc_diag, spc_off;
+};
+
+static void chunking(uint64_t total_stages, uint32_t ntiles, int num_sms, uint32_t &kc,
+                     uint64_t &spc) {
+  if (ntiles == 0) {
+    kc = 0;
+    spc = 0;
+    return;
+  }
+  uint64_t want = ((uint64_t)num_sms + ntiles - 1) / ntiles;
+  if (want < 1) want = 1;
+  if (want > total_stages) want = total_stages;
+  spc = (total_stages + want - 1) / want;
+  kc = (uint32_t)((total_stages + spc - 1) / spc);
+}
+
+static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms) {
+  Plan p{};
+  p.panel = k <= 128 ? 128 : 256;
+  p.npanels = (k + p.panel - 1) / p.panel;
+  p.ndiag = p.npanels;
+  p.noff = p.npanels * (p.npanels - 1) / 2;
+  p.total_stages = wpm / (kStagePx / 32);
+  chunking(p.total_stages, p.ndiag, num_sms, p.kc_diag, p.spc_diag);
+  chunking(p.total_stages, p.noff, num_sms, p.kc_off, p.spc_off);
+  return p;
+}
+
+}  // namespace tc
+
+size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms) {
+  tc::Plan p = tc::make_plan(k, wpm, num_sms);
+  const uint64_t per_tile = (uint64_t)p.panel * p.panel * 4;
+  return (size_t)(((uint64_t)p.ndiag * p.kc_diag + (uint64_t)p.noff * p.kc_off) * per_tile);
+}
+
+template <int PANEL, bool DIAG>
+static cudaError_t launch_one(const uint32_t *packed, uint64_t wpm, const uint32_t *slots,
+                              uint32_t k, const tc::Plan &p, int32_t *part, cudaStream_t s) {
+  using C = tc::Cfg<PANEL, DIAG>;
+  const uint32_t ntiles = DIAG ? p.ndiag : p.noff;
+  const uint32_t kc = DIAG ? p.kc_diag : p.kc_off;
+  const uint64_t spc = DIAG ? p.spc_diag : p.spc_off;
+  if (ntiles == 0 || kc == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<PANEL, DIAG>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  tc::k_gram_tc<PANEL, DIAG><<<ntiles * kc, tc::kThreads, C::kSmemBytes, s>>>(
+      packed, wpm, slots, k, p.npanels, kc, spc, p.total_stages, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t wpm, const uint32_t *slots, uint32_t k,
+                           unsigned long long *gram, void *workspace, int num_sms,
+                           cudaStream_t s) {
+  if (k == 0) return cudaSuccess;
+  tc::Plan p = tc::make_plan(k, wpm, num_sms);
+  const uint64_t per_tile = (uint64_t)p.panel * p.panel;
+  int32_t *part_diag = reinterpret_cast<int32_t *>(workspace);
+  int32_t *part_off = part_diag + (uint64_t)p.ndiag * p.kc_diag * per_tile;
+  cudaError_t e;
+  if (p.panel == 128) {
+    e = launch_one<128, true>(packed, wpm, slots, k, p, part_diag, s);
+    if (e != cudaSuccess) return e;
+    e = launch_one<128, false>(packed, wpm, slots, k, p, part_off, s);
+  } else {
+    e = launch_one<256, true>(packed, wpm, slots, k, p, part_diag, s);
+    if (e != cudaSuccess) return e;
+    e = launch_one<256, false>(packed, wpm, slots, k, p, part_off, s);
+  }
+  if (e != cudaSuccess) return e;
+  const uint64_t total = (uint64_t)(p.ndiag + p.noff) * per_tile;
+  uint64_t grid = (total + 255) / 256;
+  if (grid > (uint64_t)num_sms * 8) grid = (uint64_t)num_sms * 8;
+  if (p.panel == 128)
+    tc::k_gram_reduce<128><<<(unsigned)grid, 256, 0, s>>>(part_diag, p.kc_diag, part_off,
+                                                           p.kc_off, k, p.npanels, gram);
+  else
+    tc::k_gram_reduce<256><<<(unsigned)grid, 256, 0, s>>>(part_diag, p.kc_diag, part_off,
+                                                           p.kc_off, k, p.npanels, gram);
+  return cudaGetLastError();
+}
+
+}  // namespace fs

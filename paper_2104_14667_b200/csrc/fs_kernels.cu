@@ -1,0 +1,656 @@
+// fs_kernels.cu — per-pixel kernels of the flood-ensemble overlap path (sm_100a).
+//
+// Reference semantics (all under /root/reference/pkg/src/floodstream/):
+//   accumulate_into   _kernels_np.py:16-18   counts[p] += cells[p] > 0
+//   overlap_counts    _kernels_np.py:21-23   bins[k] = #{p : counts[p] == k}
+//   pair_counts       _kernels_np.py:26-32   (|A & B|, |A | B|) of wet masks
+//   composite_fill    _kernels_np.py:35-47   RGBA (g, g, 255, 255), g = floor(255(1-c/n)+0.5)
+//   accumulate        analytics.py:106-126   the per-surface loop, fused here
+//   transform         device.py:384-390      modelled buffer->image reorganisation; here a
+//                                            real binarize + bit-pack kernel
+// Every kernel is a streaming HBM pass: 128-bit loads, coalesced stores, persistent
+// grids sized to the SM count, shared-memory privatised histograms.
+#include <cstdio>
+#include <cmath>
+
+#include "fs_internal.h"
+
+namespace fs {
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// ---------------------------------------------------------------------------
+// bit helpers
+// ---------------------------------------------------------------------------
+// 4 bytes -> 4 bits (bit i set iff byte i != 0)
+__device__ __forceinline__ uint32_t nz_nibble(uint32_t x) {
+  uint32_t t = x | (x >> 4);
+  t |= t >> 2;
+  t |= t >> 1;
+  t &= 0x01010101u;
+  return (t * 0x00204081u) >> 21 & 0xFu;
+}
+__device__ __forceinline__ uint32_t nz_bits16(uint4 v) {
+  return nz_nibble(v.x) | (nz_nibble(v.y) << 4) | (nz_nibble(v.z) << 8) |
+         (nz_nibble(v.w) << 12);
+}
+
+__device__ __forceinline__ uint32_t grey_dev(uint64_t c, uint64_t n_inputs, const uint8_t *lut) {
+  if (lut != nullptr) return __ldg(lut + c);
+  // FP64, no contraction: sat = c / max(n,1); g = floor(255*(1-sat) + 0.5)
+  double denom = (double)(n_inputs > 0 ? n_inputs : 1);
+  double sat = __ddiv_rn((double)c, denom);
+  double g = floor(__dadd_rn(__dmul_rn(255.0, __dsub_rn(1.0, sat)), 0.5));
+  long long gi = (long long)g;
+  return (uint32_t)(gi & 0xFF);
+}
+__device__ __forceinline__ uint32_t rgba_word(uint32_t c, uint64_t n_inputs, const uint8_t *lut) {
+  if (c == 0) return 0u;
+  uint32_t g = grey_dev(c, n_inputs, lut);
+  return g | (g << 8) | 0xFFFF0000u;  // bytes (g, g, 255, 255), little endian
+}
+
+// ---------------------------------------------------------------------------
+// Transform: binarize + bit-pack, TMA bulk staged (cp.async.bulk -> SMEM ring)
+// ---------------------------------------------------------------------------
+constexpr int kPackThreads = 256;
+constexpr int kPackChunk = 8192;  // bytes (= pixels) per stage, 256 output words
+constexpr int kPackStages = 4;
+static int g_pack_engine = 0;
+void set_pack_engine(int e) { g_pack_engine = e; }
+int get_pack_engine() { return g_pack_engine; }
+
+__global__ void __launch_bounds__(kPackThreads)
+    k_pack_bulk(const uint8_t *__restrict__ src, uint64_t nchunks, uint32_t *__restrict__ dst) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm + kPackStages * kPackChunk);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kPackStages; ++s) ptx::mbar_init(&bar[s], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t nmy =
+      nchunks > blockIdx.x ? (nchunks - blockIdx.x - 1) / gridDim.x + 1 : 0;
+  if (tid == 0) {
+    for (uint64_t j = 0; j < nmy && j < (uint64_t)kPackStages; ++j) {
+      uint64_t c = blockIdx.x + j * gridDim.x;
+      ptx::mbar_arrive_expect_tx(&bar[j], kPackChunk);
+      ptx::bulk_g2s(sm + j * kPackChunk, src + c * kPackChunk, kPackChunk, &bar[j]);
+    }
+  }
+  for (uint64_t j = 0; j < nmy; ++j) {
+    const int s = (int)(j % kPackStages);
+    const uint32_t parity = (uint32_t)((j / kPackStages) & 1);
+    const uint64_t c = blockIdx.x + j * gridDim.x;
+    ptx::mbar_wait(&bar[s], parity);
+    const uint4 *stage = reinterpret_cast<const uint4 *>(sm + s * kPackChunk);
+#pragma unroll
+    for (int i = 0; i < kPackChunk / 16 / kPackThreads; ++i) {
+      const int q = tid + i * kPackThreads;
+      uint32_t h = nz_bits16(stage[q]);
+      uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
+      if ((lane & 1) == 0) dst[c * (kPackChunk / 32) + (q >> 1)] = h | (other << 16);
+    }
+    __syncthreads();
+    if (tid == 0 && j + kPackStages < nmy) {
+      uint64_t cn = blockIdx.x + (j + kPackStages) * gridDim.x;
+      ptx::mbar_arrive_expect_tx(&bar[s], kPackChunk);
+      ptx::bulk_g2s(sm + s * kPackChunk, src + cn * kPackChunk, kPackChunk, &bar[s]);
+    }
+  }
+}
+
+// Direct-load variant (no staging): each thread turns 32 bytes into one word.
+__global__ void __launch_bounds__(256)
+    k_pack_direct(const uint8_t *__restrict__ src, uint64_t nvec, uint32_t *__restrict__ dst) {
+  // nvec = number of full 16-byte vectors; pairs of lanes build one word
+  const int lane = threadIdx.x & 31;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+       q < ((nvec + 31) / 32) * 32; q += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t h = 0;
+    if (q < nvec) h = nz_bits16(ptx::ld_nc_v4(src + q * 16));
+    uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
+    if ((lane & 1) == 0 && q < nvec) dst[q >> 1] = h | (other << 16);
+  }
+}
+
+// Words [w0, wpm): scalar tail + zero padding.
+__global__ void k_pack_tail(const uint8_t *__restrict__ src, uint64_t pixels, uint64_t w0,
+                            uint64_t wpm, uint32_t *__restrict__ dst) {
+  uint64_t w = w0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (w >= wpm) return;
+  uint32_t word = 0;
+  uint64_t p0 = w * 32;
+  if (p0 < pixels) {
+    for (int b = 0; b < 32; ++b) {
+      uint64_t p = p0 + b;
+      if (p < pixels && src[p] != 0) word |= 1u << b;
+    }
+  }
+  dst[w] = word;
+}
+
+cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint64_t wpm,
+                        cudaStream_t s, int engine) {
+  if (engine < 0) engine = g_pack_engine;
+  uint64_t done_words = 0;
+  if (engine == 0) {
+    const uint64_t nchunks = pixels / kPackChunk;
+    if (nchunks > 0) {
+      static bool attr_set = false;
+      const int smem = kPackStages * kPackChunk + kPackStages * 8;
+      if (!attr_set) {
+        cudaFuncSetAttribute(k_pack_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_set = true;
+      }
+      uint64_t grid = (uint64_t)num_sms() * 6;
+      if (grid > nchunks) grid = nchunks;
+      k_pack_bulk<<<(unsigned)grid, kPackThreads, smem, s>>>(src, nchunks, dst);
+      done_words = nchunks * (kPackChunk / 32);
+    }
+  } else {
+    // full 32-byte groups only; the rest goes to the tail kernel
+    const uint64_t nvec = (pixels / 32) * 2;
+    if (nvec > 0) {
+      uint64_t threads = (nvec + 31) / 32 * 32;
+      uint64_t grid = (threads + 255) / 256;
+      uint64_t cap = (uint64_t)num_sms() * 16;
+      if (grid > cap) grid = cap;
+      k_pack_direct<<<(unsigned)grid, 256, 0, s>>>(src, nvec, dst);
+      done_words = nvec / 2;
+    }
+  }
+  if (done_words < wpm) {
+    uint64_t n = wpm - done_words;
+    k_pack_tail<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, pixels, done_words, wpm, dst);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Protocol kernels over flat arrays
+// ---------------------------------------------------------------------------
+__global__ void k_accumulate_u8(uint32_t *__restrict__ counts, const uint8_t *__restrict__ cells,
+                                uint64_t n) {
+  const uint64_t nvec = n / 16;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nvec; q += stride) {
+    uint32_t bits = nz_bits16(ptx::ld_nc_v4(cells + q * 16));
+    uint4 *c4 = reinterpret_cast<uint4 *>(counts + q * 16);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      uint4 c = c4[v];
+      c.x += (bits >> (4 * v + 0)) & 1u;
+      c.y += (bits >> (4 * v + 1)) & 1u;
+      c.z += (bits >> (4 * v + 2)) & 1u;
+      c.w += (bits >> (4 * v + 3)) & 1u;
+      c4[v] = c;
+    }
+  }
+  for (uint64_t p = nvec * 16 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
+       p += stride)
+    counts[p] += cells[p] != 0;
+}
+
+cudaError_t launch_accumulate_u8(uint32_t *counts, const uint8_t *cells, uint64_t n,
+                                 cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint64_t grid = (n / 16 + 255) / 256 + 1;
+  uint64_t cap = (uint64_t)num_sms() * 8;
+  if (grid > cap) grid = cap;
+  k_accumulate_u8<<<(unsigned)grid, 256, 0, s>>>(counts, cells, n);
+  return cudaGetLastError();
+}
+
+// Warp-aggregated histogram increment: lanes holding the same class add once.
+__device__ __forceinline__ void hist_add(uint32_t c, bool valid, uint32_t *sh,
+                                         unsigned long long *gl) {
+  const uint32_t key = valid ? c : 0xFFFFFFFFu;
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const int lane = threadIdx.x & 31;
+  if (valid && (__ffs(peers) - 1) == lane) {
+    if (sh)
+      atomicAdd(sh + c, (uint32_t)__popc(peers));
+    else
+      atomicAdd(gl + c, (unsigned long long)__popc(peers));
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_histogram(const uint32_t *__restrict__ counts, uint64_t n, uint64_t nbins,
+                unsigned long long *__restrict__ bins) {
+  __shared__ uint32_t sh[kHistSmemBins];
+  const bool use_sh = nbins <= kHistSmemBins;
+  if (use_sh)
+    for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t nvec = (n + 3) / 4;
+  const uint64_t iters = (nvec + stride - 1) / stride;
+  for (uint64_t it = 0; it < iters; ++it) {
+    uint64_t q = it * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint64_t p = q * 4 + e;
+      bool valid = p < n;
+      uint32_t c = valid ? __ldg(counts + p) : 0;
+      // counts above n_inputs would index past bins; the reference's numpy backend
+      // grows the array, the Cython one writes out of bounds.  Callers validate.
+      valid = valid && c < nbins;
+      hist_add(c, valid, use_sh ? sh : nullptr, bins);
+    }
+  }
+  __syncthreads();
+  if (use_sh)
+    for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x)
+      if (sh[i]) atomicAdd(bins + i, (unsigned long long)sh[i]);
+}
+
+cudaError_t launch_histogram(const uint32_t *counts, uint64_t n, uint64_t nbins,
+                             unsigned long long *bins, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint64_t grid = (n / 4 + 255) / 256 + 1;
+  uint64_t cap = (uint64_t)num_sms() * 4;
+  if (grid > cap) grid = cap;
+  k_histogram<<<(unsigned)grid, 256, 0, s>>>(counts, n, nbins, bins);
+  return cudaGetLastError();
+}
+
+__global__ void k_composite(const uint32_t *__restrict__ counts, uint64_t n, uint64_t n_inputs,
+                            const uint8_t *__restrict__ lut, uint32_t *__restrict__ rgba) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += stride) {
+    uint32_t c = counts[p];
+    const uint8_t *l = (lut != nullptr && c <= n_inputs) ? lut : nullptr;
+    rgba[p] = rgba_word(c, n_inputs, l);
+  }
+}
+
+cudaError_t launch_composite(const uint32_t *counts, uint64_t n, uint64_t n_inputs,
+                             const uint8_t *lut, uint32_t *rgba, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint64_t grid = (n + 255) / 256;
+  uint64_t cap = (uint64_t)num_sms() * 16;
+  if (grid > cap) grid = cap;
+  k_composite<<<(unsigned)grid, 256, 0, s>>>(counts, n, n_inputs, lut, rgba);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256)
+    k_pair_counts(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b, uint64_t n,
+                  unsigned long long *__restrict__ out) {
+  uint64_t inter = 0, uni = 0;
+  const uint64_t nvec = n / 16;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nvec; q += stride) {
+    uint32_t wa = nz_bits16(ptx::ld_nc_v4(a + q * 16));
+    uint32_t wb = nz_bits16(ptx::ld_nc_v4(b + q * 16));
+    inter += __popc(wa & wb);
+    uni += __popc(wa | wb);
+  }
+  for (uint64_t p = nvec * 16 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
+       p += stride) {
+    bool x = a[p] != 0, y = b[p] != 0;
+    inter += x && y;
+    uni += x || y;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    inter += __shfl_xor_sync(0xffffffffu, inter, o);
+    uni += __shfl_xor_sync(0xffffffffu, uni, o);
+  }
+  __shared__ unsigned long long si[8], su[8];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    si[w] = inter;
+    su[w] = uni;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ti = 0, tu = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      ti += si[i];
+      tu += su[i];
+    }
+    atomicAdd(out, ti);
+    atomicAdd(out + 1, tu);
+  }
+}
+
+cudaError_t launch_pair_counts(const uint8_t *a, const uint8_t *b, uint64_t n,
+                               unsigned long long *out2, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint64_t grid = (n / 16 + 255) / 256 + 1;
+  uint64_t cap = (uint64_t)num_sms() * 8;
+  if (grid > cap) grid = cap;
+  k_pair_counts<<<(unsigned)grid, 256, 0, s>>>(a, b, n, out2);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Fused overlap pass over bit-packed masks: bit-sliced Harley-Seal counters per
+// 32-pixel word, then counts / composite / histogram in one epilogue.
+// ---------------------------------------------------------------------------
+constexpr int kOvThreads = 128;
+constexpr int kOvNH = 12;  // high planes: 16 * (2^12 - 1) + 15 masks per pass
+
+__device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b,
+                                    uint32_t c) {
+  const uint32_t u = a ^ b;
+  h = (a & b) | (u & c);
+  l = u ^ c;
+}
+
+// Count one slot range [off, off+k) for word w into cnt[32] with weight `wt`.
+__device__ __forceinline__ void count_range(const uint32_t *__restrict__ packed, uint64_t wpm,
+                                            const uint32_t *__restrict__ slots, uint32_t off,
+                                            uint32_t k, uint64_t w, bool valid, uint32_t wt,
+                                            uint32_t (&cnt)[32]) {
+  constexpr uint32_t kGroupsPerPass = (1u << kOvNH) - 1;
+  for (uint32_t pass0 = 0; pass0 < k; pass0 += kGroupsPerPass * 16) {
+    const uint32_t kp = min(k - pass0, kGroupsPerPass * 16);
+    uint32_t ones = 0, twos = 0, fours = 0, eights = 0;
+    uint32_t H[kOvNH];
+#pragma unroll
+    for (int i = 0; i < kOvNH; ++i) H[i] = 0;
+    for (uint32_t g = 0; g < kp; g += 16) {
+      uint32_t d[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        d[j] = 0;
+        if (valid && g + j < kp) {
+          const uint32_t slot = __ldg(slots + off + pass0 + g + j);
+          d[j] = ptx::ld_nc_u32(packed + (uint64_t)slot * wpm + w);
+        }
+      }
+      uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
+      csa(twosA, ones, ones, d[0], d[1]);
+      csa(twosB, ones, ones, d[2], d[3]);
+      csa(foursA, twos, twos, twosA, twosB);
+      csa(twosA, ones, ones, d[4], d[5]);
+      csa(twosB, ones, ones, d[6], d[7]);
+      csa(foursB, twos, twos, twosA, twosB);
+      csa(eightsA, fours, fours, foursA, foursB);
+      csa(twosA, ones, ones, d[8], d[9]);
+      csa(twosB, ones, ones, d[10], d[11]);
+      csa(foursA, twos, twos, twosA, twosB);
+      csa(twosA, ones, ones, d[12], d[13]);
+      csa(twosB, ones, ones, d[14], d[15]);
+      csa(foursB, twos, twos, twosA, twosB);
+      csa(eightsB, fours, fours, foursA, foursB);
+      csa(sixteens, eights, eights, eightsA, eightsB);
+      uint32_t carry = sixteens;
+#pragma unroll
+      for (int i = 0; i < kOvNH; ++i) {
+        const uint32_t t = H[i] & carry;
+        H[i] ^= carry;
+        carry = t;
+      }
+    }
+    // extract: c = ones + 2 twos + 4 fours + 8 eights + 16 * sum_i H[i] 2^i
+    const uint32_t ngroups = (kp + 15) / 16;
+    int nh = 0;
+    while (nh < kOvNH && (ngroups >> nh) != 0) ++nh;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      uint32_t c = ((ones >> j) & 1u) | (((twos >> j) & 1u) << 1) | (((fours >> j) & 1u) << 2) |
+                   (((eights >> j) & 1u) << 3);
+#pragma unroll
+      for (int i = 0; i < kOvNH; ++i)
+        if (i < nh) c += ((H[i] >> j) & 1u) << (4 + i);
+      cnt[j] += wt * c;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kOvThreads)
+    k_overlap(const OverlapArgs a) {
+  __shared__ uint32_t sh_hist[kHistSmemBins];
+  __shared__ uint32_t tb[kOvThreads / 32][32][33];
+  const int tid = threadIdx.x;
+  const int wi = tid >> 5, lane = tid & 31;
+  const bool do_hist = a.bins != nullptr;
+  const bool sh_hist_on = do_hist && a.nbins <= kHistSmemBins;
+  if (sh_hist_on)
+    for (uint32_t i = tid; i < a.nbins; i += kOvThreads) sh_hist[i] = 0;
+  __syncthreads();
+  const uint64_t nwords = (a.pixels + 31) / 32;
+  const uint64_t ntiles = (nwords + kOvThreads - 1) / kOvThreads;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t w = tile * kOvThreads + tid;
+    const bool valid = w < nwords;
+    uint32_t cnt[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) cnt[j] = 0;
+    if (a.k1 && a.w1) count_range(a.packed, a.wpm, a.slots, 0, a.k1, w, valid, a.w1, cnt);
+    if (a.k2 && a.w2) count_range(a.packed, a.wpm, a.slots, a.k1, a.k2, w, valid, a.w2, cnt);
+    // transpose through SMEM so that stores are lane-contiguous
+#pragma unroll
+    for (int j = 0; j < 32; ++j) tb[wi][lane][j] = cnt[j];
+    __syncwarp();
+    const uint64_t wbase = tile * kOvThreads + (uint64_t)wi * 32;
+    for (int i = 0; i < 32; ++i) {
+      const uint64_t px = (wbase + i) * 32 + lane;
+      const bool pv = px < a.pixels;
+      const uint32_t c = tb[wi][i][lane];
+      if (pv) {
+        if (a.counts) a.counts[px] = c;
+        if (a.rgba) a.rgba[px] = rgba_word(c, a.n_inputs, a.lut);
+      }
+      if (do_hist) hist_add(c, pv && c < a.nbins, sh_hist_on ? sh_hist : nullptr, a.bins);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (sh_hist_on)
+    for (uint32_t i = tid; i < a.nbins; i += kOvThreads)
+      if (sh_hist[i]) atomicAdd(a.bins + i, (unsigned long long)sh_hist[i]);
+}
+
+cudaError_t launch_overlap(const OverlapArgs &a, cudaStream_t s) {
+  if (a.pixels == 0) return cudaSuccess;
+  const uint64_t nwords = (a.pixels + 31) / 32;
+  const uint64_t ntiles = (nwords + kOvThreads - 1) / kOvThreads;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_overlap, kOvThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = (uint64_t)num_sms() * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  k_overlap<<<(unsigned)grid, kOvThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// Per-item streaming accumulate (run_stream's kernel[i]): counts += bits of one mask.
+__global__ void k_accumulate_packed(const uint32_t *__restrict__ pk, uint64_t pixels,
+                                    uint32_t *__restrict__ counts) {
+  const uint64_t nwords = (pixels + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w0 = warp * 32; w0 < nwords; w0 += nwarps * 32) {
+    const uint32_t mine = (w0 + lane < nwords) ? ptx::ld_nc_u32(pk + w0 + lane) : 0u;
+    for (int i = 0; i < 32; ++i) {
+      const uint32_t wd = __shfl_sync(0xffffffffu, mine, i);
+      const uint64_t px = (w0 + i) * 32 + lane;
+      if (px < pixels) counts[px] += (wd >> lane) & 1u;
+    }
+  }
+}
+
+cudaError_t launch_accumulate_packed(const uint32_t *packed_mask, uint64_t pixels,
+                                     uint32_t *counts, cudaStream_t s) {
+  if (pixels == 0) return cudaSuccess;
+  const uint64_t nwords = (pixels + 31) / 32;
+  uint64_t grid = (nwords + 255) / 256;
+  uint64_t cap = (uint64_t)num_sms() * 8;
+  if (grid > cap) grid = cap;
+  k_accumulate_packed<<<(unsigned)grid, 256, 0, s>>>(packed_mask, pixels, counts);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Gram on CUDA cores: AND + POPC over bit-packed masks (baseline engine)
+// ---------------------------------------------------------------------------
+constexpr int kGpTile = 64;
+constexpr int kGpSlab = 32;
+
+__global__ void __launch_bounds__(256)
+    k_gram_popc(const uint32_t *__restrict__ packed, uint64_t wpm,
+                const uint32_t *__restrict__ slots, uint32_t k, uint32_t nb, uint64_t kchunk,
+                unsigned long long *__restrict__ gram) {
+  __shared__ uint32_t A[kGpTile][kGpSlab + 1];
+  __shared__ uint32_t B[kGpTile][kGpSlab + 1];
+  // upper-triangular tile index -> (I, J)
+  uint32_t t = blockIdx.x, I = 0;
+  while (t >= nb - I) {
+    t -= nb - I;
+    ++I;
+  }
+  const uint32_t J = I + t;
+  const uint64_t k0 = (uint64_t)blockIdx.y * kchunk;
+  const uint64_t k1 = min(k0 + kchunk, wpm);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  uint32_t acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+  for (uint64_t kb = k0; kb < k1; kb += kGpSlab) {
+    for (int idx = threadIdx.x; idx < kGpTile * kGpSlab; idx += 256) {
+      const int r = idx / kGpSlab, c = idx % kGpSlab;
+      const uint32_t ra = I * kGpTile + r, rb = J * kGpTile + r;
+      const bool kin = kb + c < k1;
+      A[r][c] = (ra < k && kin) ? __ldg(packed + (uint64_t)__ldg(slots + ra) * wpm + kb + c) : 0u;
+      B[r][c] = (rb < k && kin) ? __ldg(packed + (uint64_t)__ldg(slots + rb) * wpm + kb + c) : 0u;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int c = 0; c < kGpSlab; ++c) {
+      uint32_t av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = A[ty * 4 + i][c];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = B[tx * 4 + j][c];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += __popc(av[i] & bv[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t r = I * kGpTile + ty * 4 + i, c = J * kGpTile + tx * 4 + j;
+      if (r < k && c < k && acc[i][j]) atomicAdd(gram + (uint64_t)r * k + c, (unsigned long long)acc[i][j]);
+    }
+}
+
+cudaError_t launch_gram_popc(const uint32_t *packed, uint64_t wpm, const uint32_t *slots,
+                             uint32_t k, unsigned long long *gram, cudaStream_t s) {
+  if (k == 0) return cudaSuccess;
+  const uint32_t nb = (k + kGpTile - 1) / kGpTile;
+  const uint32_t ntiles = nb * (nb + 1) / 2;
+  uint64_t want = (uint64_t)num_sms() * 4;
+  uint64_t ksplit = (want + ntiles - 1) / ntiles;
+  uint64_t kchunk = (wpm + ksplit - 1) / ksplit;
+  kchunk = (kchunk + kGpSlab - 1) / kGpSlab * kGpSlab;
+  if (kchunk == 0) kchunk = kGpSlab;
+  ksplit = (wpm + kchunk - 1) / kchunk;
+  if (ksplit > 65535) {
+    ksplit = 65535;
+    kchunk = ((wpm + ksplit - 1) / ksplit + kGpSlab - 1) / kGpSlab * kGpSlab;
+  }
+  dim3 grid(ntiles, (unsigned)ksplit);
+  k_gram_popc<<<grid, 256, 0, s>>>(packed, wpm, slots, k, nb, kchunk, gram);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_gram_mirror(gram, k, kGpTile, s);
+}
+
+// Fill entries of lower tiles from their mirror (tile size `tile`).
+__global__ void k_gram_mirror(unsigned long long *gram, uint32_t k, uint32_t tile) {
+  const uint64_t n = (uint64_t)k * k;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(e / k), j = (uint32_t)(e % k);
+    if (i / tile > j / tile) gram[e] = gram[(uint64_t)j * k + i];
+  }
+}
+
+cudaError_t launch_gram_mirror(unsigned long long *gram, uint32_t k, uint32_t tile,
+                               cudaStream_t s) {
+  if (k <= tile) return cudaSuccess;
+  uint64_t n = (uint64_t)k * k;
+  uint64_t grid = (n + 255) / 256;
+  if (grid > 4096) grid = 4096;
+  k_gram_mirror<<<(unsigned)grid, 256, 0, s>>>(gram, k, tile);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic masks generated straight into the packed layout
+// ---------------------------------------------------------------------------
+__global__ void k_synth_packed(uint32_t *__restrict__ dst, uint64_t wpm, SynthParams sp,
+                               uint64_t mask, uint64_t row0, uint64_t pixels) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < wpm; w += stride) {
+    uint32_t word = 0;
+    const uint64_t p0 = w * 32;
+    if (p0 < pixels) {
+      uint64_t y = row0 + p0 / sp.width;
+      uint32_t x = (uint32_t)(p0 % sp.width);
+      for (int b = 0; b < 32; ++b) {
+        if (p0 + b >= pixels) break;
+        if (synth_cell(sp, mask, (uint32_t)y, x) != 0) word |= 1u << b;
+        if (++x == sp.width) {
+          x = 0;
+          ++y;
+        }
+      }
+    }
+    dst[w] = word;
+  }
+}
+
+cudaError_t launch_synth_packed(uint32_t *dst, uint64_t wpm, const SynthParams &sp,
+                                uint64_t mask, uint64_t row0, uint64_t pixels,
+                                cudaStream_t s) {
+  uint64_t grid = (wpm + 255) / 256;
+  uint64_t cap = (uint64_t)num_sms() * 16;
+  if (grid > cap) grid = cap;
+  k_synth_packed<<<(unsigned)grid, 256, 0, s>>>(dst, wpm, sp, mask, row0, pixels);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Host: composite grey LUT, evaluated exactly like _kernels_np.py:41-42 in FP64.
+// This translation unit is compiled with -ffp-contract=off for host code.
+// ---------------------------------------------------------------------------
+uint8_t grey_of(uint64_t c, uint64_t n_inputs) {
+  volatile double denom = (double)(n_inputs > 0 ? n_inputs : 1);
+  volatile double sat = (double)c / denom;
+  volatile double one_minus = 1.0 - sat;
+  volatile double scaled = 255.0 * one_minus;
+  volatile double shifted = scaled + 0.5;
+  double g = std::floor(shifted);
+  long long gi = (long long)g;
+  return (uint8_t)(gi & 0xFF);
+}
+
+void build_grey_lut(uint64_t n_inputs, uint8_t *lut, uint64_t entries) {
+  for (uint64_t c = 0; c < entries; ++c) lut[c] = grey_of(c, n_inputs);
+}
+
+}  // namespace fs

@@ -1,0 +1,259 @@
+"""Device-resident flood ensemble: bit-packed masks kept in HBM.
+
+The interactive-recompute target (≥10 FPS over 256 × 8192² masks) cannot re-stream
+17 GB over PCIe every frame, so the masks are uploaded once — through the paper's
+dual-buffer pipeline — binarized and bit-packed (P/8 bytes per mask), and every
+recompute reads them from HBM:
+
+* ``overlap()``  — counts + histogram + composite in one fused pass
+  (analytics.py:106-162 on the reference side);
+* ``gram()``     — exact pairwise intersections on tcgen05 int8 tensor cores
+  (the pair_counts loop of analytics.py:174-181);
+* ``recompute()``— the service snapshot (service.py:143-175) plus the /clusters and
+  /outliers products (service.py:289-307) from one overlap pass and one Gram.
+
+A ``DeviceEnsemble`` may hold a horizontal *band* of every mask (rows
+[row0, row0 + rows)); bands are how the multi-GPU path shards pixels (see dist.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .analytics import (
+    AccumulationGrid,
+    CompositeImage,
+    OverlapHistogram,
+    cluster_from_similarity,
+    outliers_from_similarity,
+    similarity_from_gram,
+)
+
+_GRAM_ENGINES = {"auto": N.GRAM_AUTO, "popc": N.GRAM_POPC, "tc": N.GRAM_TC_I8, "tc-i8": N.GRAM_TC_I8}
+
+
+@dataclass
+class StreamStats:
+    """Measured timings of one streamed upload (µs, CUDA events / host clock)."""
+
+    variant: str
+    n: int
+    total_us: float
+    host_us: list[float] = field(default_factory=list)
+    copy_us: list[float] = field(default_factory=list)
+    xform_us: list[float] = field(default_factory=list)
+    kernel_us: list[float] = field(default_factory=list)
+
+
+@dataclass
+class Snapshot:
+    """One full recompute of the working set."""
+
+    grid: AccumulationGrid | None
+    histogram: OverlapHistogram | None
+    composite: CompositeImage | None
+    gram: np.ndarray | None
+    similarity: np.ndarray | None
+    outliers: dict | None
+    clusters: list | None
+
+
+class DeviceEnsemble:
+    """Bit-packed masks of one raster size (or one row band of it) resident in HBM."""
+
+    def __init__(self, width: int, height: int, capacity: int, *, row0: int = 0,
+                 rows: int | None = None, device: int | None = None):
+        if rows is None:
+            rows = height - row0
+        if width < 1 or height < 1 or rows < 1 or row0 < 0 or row0 + rows > height:
+            raise ValueError("bad ensemble geometry")
+        if device is not None:
+            N.set_device(device)
+        self.width, self.height, self.row0, self.rows = int(width), int(height), int(row0), int(rows)
+        self.pixels = self.width * self.rows
+        self.capacity = int(capacity)
+        h = C.c_void_p()
+        N.call("fs_ensemble_create", self.pixels, self.capacity, C.byref(h))
+        self._h = h
+        wpm, dev = C.c_uint64(), C.c_int()
+        N.call("fs_ensemble_info", self._h, None, None, C.byref(wpm), C.byref(dev))
+        self.words_per_mask = wpm.value
+        self.device = dev.value
+        self.ids: list[str | None] = [None] * self.capacity
+
+    # -- lifetime -------------------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            N.load().fs_ensemble_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- helpers --------------------------------------------------------------------
+    def _slots(self, slots) -> np.ndarray:
+        if slots is None:
+            slots = [i for i, s in enumerate(self.ids) if s is not None] or range(self.capacity)
+        a = np.ascontiguousarray(np.asarray(list(slots) if not isinstance(slots, np.ndarray) else slots,
+                                            dtype=np.uint32))
+        if a.size == 0:
+            raise ValueError("need at least one slot")
+        return a
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def stream_handle(self) -> int:
+        p = C.c_void_p()
+        N.call("fs_ensemble_stream_handle", self._h, C.byref(p))
+        return p.value or 0
+
+    def sync(self) -> None:
+        N.call("fs_ensemble_sync", self._h)
+
+    def kernel_ms(self, kind: str) -> float:
+        code = {"pack": N.KERNEL_PACK, "overlap": N.KERNEL_OVERLAP, "gram": N.KERNEL_GRAM}[kind]
+        ms = C.c_float()
+        N.call("fs_ensemble_kernel_ms", self._h, code, C.byref(ms))
+        return float(ms.value)
+
+    # -- filling --------------------------------------------------------------------
+    def band_view(self, cells: np.ndarray) -> np.ndarray:
+        """This ensemble's rows of a full (H, W) raster, as a flat contiguous array."""
+        a = cells.reshape(self.height, self.width)[self.row0:self.row0 + self.rows]
+        return np.ascontiguousarray(a).reshape(-1)
+
+    def stream(self, rasters, *, first: int = 0, variant: str = "2b-final",
+               with_kernel: bool = False, reset_counts: bool = True, slot_wrap: int = 0,
+               ids=None, already_banded: bool = False) -> StreamStats:
+        """Upload rasters (uint8 arrays of this ensemble's band) through the variant's
+        pipeline; slot of item i = first + (i % slot_wrap or i)."""
+        arrays = []
+        for r in rasters:
+            a = getattr(r, "cells", r)
+            if not already_banded and (self.row0 != 0 or self.rows != self.height):
+                a = self.band_view(a)
+            a = a.reshape(-1)
+            if a.dtype != np.uint8 or a.size != self.pixels:
+                raise ValueError(f"raster must be uint8 with {self.pixels} pixels")
+            if not a.flags["C_CONTIGUOUS"]:
+                a = np.ascontiguousarray(a)
+            arrays.append(a)
+        k = len(arrays)
+        items = (N.StreamItem * max(k, 1))()
+        rep = N.StreamReport(0.0, k, items)
+        code = N.VARIANT_CODES[variant]
+        N.call("fs_ensemble_stream", self._h, first, slot_wrap, N.ptr_array(arrays), k, code,
+               int(with_kernel), int(reset_counts), C.byref(rep))
+        span = min(slot_wrap, k) if slot_wrap else k
+        for i in range(span):
+            self.ids[first + i] = (ids[i] if ids is not None else
+                                   getattr(rasters[i], "id", f"slot{first + i}"))
+        return StreamStats(
+            variant=variant, n=k, total_us=rep.total_us,
+            host_us=[items[i].host_us for i in range(k)],
+            copy_us=[items[i].copy_us for i in range(k)],
+            xform_us=[items[i].xform_us for i in range(k)],
+            kernel_us=[items[i].kernel_us for i in range(k)],
+        )
+
+    def upload(self, surfaces, *, first: int = 0, variant: str | None = None) -> StreamStats:
+        """Upload surfaces into slots first.. (2b-final when the sources are pinned,
+        2b-initial — pinned staging with a parallel host copy — when pageable)."""
+        if variant is None:
+            pinned = all(N.is_pinned(getattr(s, "cells", s)) for s in surfaces)
+            variant = "2b-final" if pinned else "2b-initial"
+        return self.stream(surfaces, first=first, variant=variant)
+
+    def synth(self, first: int, k: int, *, seed: int, members: int, eps: float,
+              mask_index0: int | None = None) -> None:
+        """Generate flood-like synthetic masks (fs_synth_host's bytes) straight into
+        slots first..first+k-1, for this ensemble's band."""
+        mi = first if mask_index0 is None else mask_index0
+        N.call("fs_ensemble_synth", self._h, first, k, seed, self.width, self.height, self.row0,
+               members, float(eps), mi)
+        for i in range(k):
+            self.ids[first + i] = f"s{mi + i:04d}"
+
+    # -- recompute ------------------------------------------------------------------
+    def overlap(self, slots=None, *, cycles: int = 1, remainder: int = 0, counts: bool = True,
+                bins: bool = True, rgba: bool = True, out_counts=None, out_rgba=None,
+                out_bins=None, device_outputs: bool = False):
+        """Fused counts / histogram / composite over ``slots`` (cycled to
+        n = cycles*k + remainder).  Returns (counts[H_band, W], bins, rgba[H_band, W, 4])
+        as numpy arrays (or the device pointers passed in when device_outputs)."""
+        sl = self._slots(slots)
+        k = int(sl.size)
+        n_inputs = cycles * k + remainder
+        if device_outputs:
+            cp = int(out_counts) if (counts and out_counts is not None) else None
+            rp = int(out_rgba) if (rgba and out_rgba is not None) else None
+            bp = int(out_bins) if (bins and out_bins is not None) else None
+            N.call("fs_ensemble_overlap", self._h, sl.ctypes.data_as(N._u32p), k, cycles,
+                   remainder, cp, bp, rp, 1)
+            return out_counts, out_bins, out_rgba
+        c = (out_counts if out_counts is not None else
+             np.empty((self.rows, self.width), dtype=np.uint32)) if counts else None
+        r = (out_rgba if out_rgba is not None else
+             np.empty((self.rows, self.width, 4), dtype=np.uint8)) if rgba else None
+        b = (out_bins if out_bins is not None else
+             np.empty(n_inputs + 1, dtype=np.int64)) if bins else None
+        N.call("fs_ensemble_overlap", self._h, sl.ctypes.data_as(N._u32p), k, cycles, remainder,
+               None if c is None else N.ptr(c), None if b is None else N.ptr(b),
+               None if r is None else N.ptr(r), 0)
+        return c, b, r
+
+    def running_counts(self, n_inputs: int, *, bins: bool = True, rgba: bool = True):
+        c = np.empty((self.rows, self.width), dtype=np.uint32)
+        b = np.empty(n_inputs + 1, dtype=np.int64) if bins else None
+        r = np.empty((self.rows, self.width, 4), dtype=np.uint8) if rgba else None
+        N.call("fs_ensemble_running_counts", self._h, N.ptr(c), None if b is None else N.ptr(b),
+               None if r is None else N.ptr(r), n_inputs, 0)
+        return c, b, r
+
+    def gram(self, slots=None, *, engine: str = "auto", out=None, device_outputs: bool = False):
+        """int64 (k, k) intersection Gram of the slots' wet masks (this band's pixels)."""
+        sl = self._slots(slots)
+        k = int(sl.size)
+        if device_outputs:
+            N.call("fs_ensemble_gram", self._h, sl.ctypes.data_as(N._u32p), k,
+                   _GRAM_ENGINES[engine], int(out), 1)
+            return out
+        g = out if out is not None else np.empty((k, k), dtype=np.int64)
+        N.call("fs_ensemble_gram", self._h, sl.ctypes.data_as(N._u32p), k, _GRAM_ENGINES[engine],
+               N.ptr(g), 0)
+        return g
+
+    def recompute(self, slots=None, *, tau: float = 0.8, engine: str = "auto",
+                  overlap: bool = True, pairwise: bool = True) -> Snapshot:
+        """Full recompute of the working set: grid, histogram, composite, Gram,
+        similarity, outlier scores and clusters."""
+        sl = self._slots(slots)
+        ids = [self.ids[i] if self.ids[i] is not None else f"slot{i}" for i in sl.tolist()]
+        grid = hist = comp = gram = sim = outl = clus = None
+        if overlap:
+            c, b, r = self.overlap(sl)
+            grid = AccumulationGrid._from_device(self.width, self.rows, int(sl.size), c)
+            hist = OverlapHistogram(bins=[int(x) for x in b])
+            comp = CompositeImage(width=self.width, height=self.rows, pixels=r)
+        if pairwise:
+            gram = self.gram(sl, engine=engine)
+            sim = similarity_from_gram(gram)
+            if len(ids) >= 2:
+                outl = outliers_from_similarity(sim, ids)
+            clus = cluster_from_similarity(sim, ids, tau)
+        return Snapshot(grid, hist, comp, gram, sim, outl, clus)

@@ -1,0 +1,277 @@
+"""GPU parity: every CUDA path against the oracle and the reference's golden vectors.
+
+Bit-exact for counts, histograms, RGBA, Gram; float64 results (Jaccard, outliers) must
+be identical to the reference's because they are computed from the same exact integers
+with the same operation order.  All calls go through the product package / C ABI.
+"""
+
+import numpy as np
+import pytest
+
+from golden_inputs import c1_cells, edge_cases, random_case, sha, stream_case
+from oracle import fs_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2104_14667_b200 as fs  # noqa: E402
+from paper_2104_14667_b200 import _kernels_cuda as K  # noqa: E402
+from paper_2104_14667_b200 import _native as N  # noqa: E402
+from paper_2104_14667_b200.ensemble import DeviceEnsemble  # noqa: E402
+from paper_2104_14667_b200.rasters import RasterSurface  # noqa: E402
+from paper_2104_14667_b200.synth import synth_cells  # noqa: E402
+
+
+def surfaces_of(cells, ids=None):
+    return [RasterSurface(id=(ids[i] if ids else f"s{i:02d}"), name="x", width=c.shape[1],
+                          height=c.shape[0], cells=c) for i, c in enumerate(cells)]
+
+
+def test_backend_is_cuda():
+    assert fs.analytics.kernels.NAME == "cuda"
+    assert N.device_count() >= 1
+
+
+# ---- protocol primitives ------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 31, 32, 33, 4095, 4096, 8191, 8192, 8193,
+                               100_003, 1 << 20])
+def test_primitives_match_oracle(n):
+    rng = np.random.default_rng(n)
+    a = (rng.integers(0, 4, n)).astype(np.uint8)
+    b = (rng.random(n) < 0.3).astype(np.uint8) * 200
+    counts = rng.integers(0, 5, n).astype(np.uint32)
+    want = counts.copy()
+    O.accumulate_into(want, a)
+    K.accumulate_into(counts, a)
+    assert np.array_equal(counts, want)
+    assert np.array_equal(K.overlap_counts(counts, 5), O.overlap_counts(counts, 5))
+    assert K.pair_counts(a, b) == O.pair_counts(a, b)
+    o1 = np.zeros((n, 4), np.uint8)
+    o2 = np.zeros((n, 4), np.uint8)
+    K.composite_fill(counts, 5, o1)
+    O.composite_fill(counts, 5, o2)
+    assert np.array_equal(o1, o2)
+
+
+@pytest.mark.parametrize("n_inputs", [0, 1, 2, 3, 7, 255, 256, 1000, 4095, 4096, 10_000,
+                                      (1 << 20) + 5])
+def test_composite_and_histogram_all_classes(n_inputs):
+    c = np.arange(min(n_inputs, 300_000) + 1, dtype=np.uint32)
+    c = np.concatenate([c, c[::-1], np.full(33, min(n_inputs, c[-1]), np.uint32)])
+    o1 = np.zeros((c.size, 4), np.uint8)
+    o2 = np.zeros((c.size, 4), np.uint8)
+    K.composite_fill(c, n_inputs, o1)
+    O.composite_fill(c, n_inputs, o2)
+    assert np.array_equal(o1, o2)
+    assert np.array_equal(K.overlap_counts(c, n_inputs), O.overlap_counts(c, n_inputs))
+
+
+def test_protocol_backend_parity_reference_case():
+    """test_analytics.py:261-285 inputs (seed 11, 4096 px, p = 0.4) vs the oracle."""
+    rng = np.random.default_rng(11)
+    cells = (rng.random(4096) < 0.4).astype(np.uint8)
+    other = (rng.random(4096) < 0.4).astype(np.uint8)
+    got, want = np.zeros(4096, np.uint32), np.zeros(4096, np.uint32)
+    for x in (cells, other):
+        K.accumulate_into(got, x)
+        O.accumulate_into(want, x)
+    assert np.array_equal(got, want)
+    o1, o2 = np.zeros((4096, 4), np.uint8), np.zeros((4096, 4), np.uint8)
+    K.composite_fill(got, 2, o1)
+    O.composite_fill(want, 2, o2)
+    assert np.array_equal(o1, o2)
+    assert K.pair_counts(cells, other) == O.pair_counts(cells, other)
+    assert np.array_equal(K.overlap_counts(got, 2), O.overlap_counts(want, 2))
+
+
+# ---- analytics against golden vectors --------------------------------------------------
+
+def _check_analytics(rec, cells, ids, taus):
+    s = surfaces_of(cells, ids)
+    grid = fs.accumulate(s)
+    assert sha(grid.counts) == rec["counts_sha"]
+    assert grid.digest() == rec["digest"]
+    assert fs.overlap_histogram(grid).bins == rec["bins"]
+    assert sha(fs.composite_map(grid).pixels) == rec["composite_sha"]
+    sim = fs.similarity_matrix(s)
+    assert sha(sim) == rec["sim_sha"]
+    for t in taus:
+        assert fs.cluster_surfaces(s, t) == rec["clusters"][repr(t)]
+    if len(s) >= 2:
+        got = {k: float(v).hex() for k, v in fs.outlier_scores(s).items()}
+        assert got == rec["outliers"]
+
+
+def test_c1_goldens(golden):
+    rec = golden["c1"]
+    _check_analytics(rec, c1_cells(), rec["ids"], [0.8, 0.3])
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_random_goldens(golden, case):
+    cells, ids, tau = random_case(case)
+    _check_analytics(golden["random"][case], cells, ids, [tau])
+
+
+@pytest.mark.parametrize("name", sorted(edge_cases()))
+def test_edge_goldens(golden, name):
+    cells, ids, taus = edge_cases()[name]
+    _check_analytics(golden["edge"][name], cells, ids, taus)
+
+
+def test_jaccard_pairs_match_reference(golden):
+    cells, ids, _ = random_case(1)
+    s = surfaces_of(cells, ids)
+    g = np.array(golden["random"][1]["gram"])
+    for i in range(len(s)):
+        for j in range(len(s)):
+            inter = int(g[i, j])
+            union = int(g[i, i]) + int(g[j, j]) - inter
+            assert fs.jaccard(s[i], s[j]) == O.jaccard_from_counts(inter, union)
+
+
+# ---- streaming ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", range(6))
+@pytest.mark.parametrize("variant", [v.value for v in fs.Variant])
+def test_run_stream_goldens(golden, case, variant):
+    rec = golden["stream"][case]
+    cells, n = stream_case(case)
+    h, w = cells[0].shape
+    job = fs.StreamJob(variant=fs.Variant(variant), n=n, width=w, height=h,
+                       surfaces=surfaces_of(cells))
+    grid, report = fs.run_stream(job)
+    assert grid.digest() == rec["digest"]
+    assert fs.overlap_histogram(grid).bins == rec["bins"]
+    assert sha(fs.composite_map(grid).pixels) == rec["composite_sha"]
+    assert report.n == n and len(report.per_item_c) == n
+    assert report.total_time_us >= 1 and report.makespan_source == "measured"
+    assert all(x >= 0 for x in report.per_item_c + report.per_item_m + report.per_item_p)
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_ensemble_cycled_overlap(golden, case):
+    """Fused overlap with cycles/remainder == run_stream's cycled grid (streaming.py:417)."""
+    rec = golden["stream"][case]
+    cells, n = stream_case(case)
+    h, w = cells[0].shape
+    k = len(cells)
+    with DeviceEnsemble(w, h, k) as ens:
+        ens.upload(cells)
+        cyc, rem = divmod(n, k)
+        c, b, r = ens.overlap(list(range(k)), cycles=cyc, remainder=rem)
+    assert O.grid_digest(w, h, n, c) == rec["digest"]
+    assert b.tolist() == rec["bins"]
+    assert sha(r) == rec["composite_sha"]
+
+
+# ---- Gram engines ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("engine", ["popc", "tc"])
+@pytest.mark.parametrize("k,h,w", [(1, 3, 5), (2, 1, 1), (16, 64, 64), (31, 17, 129),
+                                   (128, 32, 32), (129, 40, 33), (200, 64, 80),
+                                   (256, 32, 64), (257, 16, 33), (300, 24, 40)])
+def test_gram_engines_exact(engine, k, h, w):
+    rng = np.random.default_rng(k * 1000 + h)
+    cells = [(rng.random((h, w)) < rng.uniform(0.05, 0.95)).astype(np.uint8) for _ in range(k)]
+    if k > 3:
+        cells[3] = cells[0].copy()
+    want = O.gram(cells)
+    with DeviceEnsemble(w, h, k) as ens:
+        ens.upload(cells)
+        got = ens.gram(list(range(k)), engine=engine)
+        # permuted / repeated slot lists
+        perm = rng.permutation(k)
+        got_p = ens.gram(perm.tolist(), engine=engine)
+    assert np.array_equal(got, want)
+    assert np.array_equal(got_p, want[np.ix_(perm, perm)])
+
+
+@pytest.mark.parametrize("engine", ["popc", "tc"])
+def test_gram_large_pixels(engine):
+    """Many K stages and K chunks: 24 flood-like masks of 1536 x 1100 px."""
+    cells = [synth_cells(1100, 1536, i, members=6, eps=0.05) for i in range(24)]
+    want = O.gram(cells)
+    with DeviceEnsemble(1100, 1536, 24) as ens:
+        ens.upload(cells)
+        got = ens.gram(engine=engine)
+    assert np.array_equal(got, want)
+
+
+# ---- transform, synth ------------------------------------------------------------------
+
+@pytest.mark.parametrize("pixels", [1, 31, 8191, 8192, 8193, 3 * 8192 + 17, 1 << 20, 612 * 499])
+@pytest.mark.parametrize("engine", [0, 1])
+def test_pack_engines(pixels, engine):
+    rng = np.random.default_rng(pixels)
+    cells = [rng.integers(0, 3, pixels).astype(np.uint8).reshape(1, pixels) for _ in range(3)]
+    N.call("fs_set_pack_engine", engine)
+    try:
+        with DeviceEnsemble(pixels, 1, 3) as ens:
+            ens.upload(cells)
+            c, b, r = ens.overlap([0, 1, 2])
+            g = ens.gram([0, 1, 2], engine="popc")
+    finally:
+        N.call("fs_set_pack_engine", 0)
+    want = O.accumulate(cells, pixels, 1)
+    assert np.array_equal(c, want)
+    assert np.array_equal(g, O.gram(cells))
+
+
+def test_device_synth_equals_host_synth():
+    w, h = 1000, 777
+    with DeviceEnsemble(w, h, 5) as dev_ens, DeviceEnsemble(w, h, 5) as host_ens:
+        dev_ens.synth(0, 5, seed=2104, members=2, eps=0.03, mask_index0=10)
+        host = [synth_cells(w, h, 10 + i, seed=2104, members=2, eps=0.03) for i in range(5)]
+        host_ens.upload(host)
+        a = dev_ens.overlap()
+        b = host_ens.overlap()
+        assert np.array_equal(a[0], b[0])
+        assert np.array_equal(dev_ens.gram(engine="tc"), host_ens.gram(engine="popc"))
+    assert np.array_equal(a[0], O.accumulate(host, w, h))
+
+
+def test_band_ensembles_tile_the_raster():
+    """Row bands (the multi-GPU shard) reassemble to the full result."""
+    w, h, k = 300, 97, 7
+    cells = [synth_cells(w, h, i, members=3) for i in range(k)]
+    full = O.accumulate(cells, w, h)
+    g = np.zeros((k, k), np.int64)
+    bins = np.zeros(k + 1, np.int64)
+    parts = []
+    for row0, rows in [(0, 30), (30, 40), (70, 27)]:
+        with DeviceEnsemble(w, h, k, row0=row0, rows=rows) as ens:
+            ens.upload(cells)
+            c, b, _ = ens.overlap()
+            parts.append(c)
+            bins += b
+            g += ens.gram()
+    assert np.array_equal(np.concatenate(parts), full)
+    assert np.array_equal(bins, O.overlap_counts(full.reshape(-1), k))
+    assert np.array_equal(g, O.gram(cells))
+
+
+# ---- full-size properties ------------------------------------------------------------
+
+def test_c2_scale_properties():
+    """256 masks of 8192 x 8192 (config 2), device-generated: size-independent
+    invariants — histogram mass, count mass = Gram trace, composite consistency, and
+    exact agreement of the two Gram engines."""
+    w = h = 8192
+    k = 256
+    with DeviceEnsemble(w, h, k) as ens:
+        ens.synth(0, k, seed=2104, members=16, eps=0.02)
+        c, b, r = ens.overlap()
+        g_tc = ens.gram(engine="tc")
+        g_pc = ens.gram(engine="popc")
+    assert np.array_equal(g_tc, g_pc)
+    assert int(b.sum()) == w * h
+    assert int(c.sum(dtype=np.uint64)) == int(np.trace(g_tc))
+    assert np.array_equal(b, np.bincount(c.reshape(-1), minlength=k + 1))
+    idx = np.random.default_rng(0).integers(0, w * h, 200_000)
+    cc = c.reshape(-1)[idx]
+    want = np.zeros((idx.size, 4), np.uint8)
+    O.composite_fill(cc, k, want)
+    assert np.array_equal(r.reshape(-1, 4)[idx], want)
+    sim = fs.similarity_from_gram(g_tc)
+    assert np.array_equal(sim, O.similarity_from_gram(g_tc))
