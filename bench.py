@@ -52,7 +52,7 @@ CONFIGS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
@@ -68,56 +68,61 @@ def parse():
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 class Clocks:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and clock-event (throttle) reasons during the timed region:
+    NVML every ~5 ms on a background thread (nvidia-smi -lms is too coarse for a
+    region of tens of milliseconds)."""
 
-    def __init__(self, gpu_index: int):
+    REASONS = {
+        "hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+        "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, gpu_index: int, period_s: float = 0.005):
         self.idx = gpu_index
-        self.proc = None
-        self.lines: list[str] = []
+        self.period = period_s
+        self.sm: list[float] = []
+        self.max_sm = None
+        self.reasons: set[str] = set()
+        self._stop = threading.Event()
+        self._ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+            self._ok = True
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         except Exception:
-            self.proc = None
+            self._ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._ok:
+            self._t.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": self.max_sm, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml"}
 
 
 def measured_peaks() -> dict:
@@ -314,7 +319,10 @@ def main():
 
     ens = DeviceEnsemble(width, height, k, row0=row0, rows=rows)
     ens.synth(0, k, seed=2104, members=members, eps=eps)
-    stream = torch.cuda.ExternalStream(ens.stream_handle())
+    # the ensemble's compute work runs on a torch-owned stream, so collectives, copies
+    # and timing events are ordered with it and its lifetime is torch's
+    stream = torch.cuda.Stream()
+    ens.use_stream(stream.cuda_stream)
     dev = torch.device("cuda", local_rank)
     d_counts = torch.empty(P_band, dtype=torch.int32, device=dev)
     d_rgba = torch.empty(P_band * 4, dtype=torch.uint8, device=dev)
@@ -479,6 +487,11 @@ def main():
             gram_launches = 1 + (1 if k > 64 else 0)  # popc, mirror
         line["gpu_launches"] = (1 + gram_launches) * args.steps
         print(json.dumps(line), flush=True)
+    torch.cuda.synchronize()
+    ens.close()
+    if e2e is not None:
+        for b in host + [h_counts, h_rgba]:
+            b.free()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -96,7 +96,8 @@ int fs_ensemble_create(uint64_t pixels, uint32_t capacity, fs_ensemble **out);
 int fs_ensemble_destroy(fs_ensemble *ens);
 int fs_ensemble_info(const fs_ensemble *ens, uint64_t *pixels, uint32_t *capacity,
                      uint64_t *words_per_mask, int *device);
-/* Device pointer to the packed masks, [capacity][words_per_mask] uint32 LSB-first. */
+/* Device pointer to the packed masks: tile-interleaved, word w of slot s at
+ * ((w / 32) * capacity + s) * 32 + w % 32, pixel 32*w + b in bit b (LSB first).     */
 int fs_ensemble_packed_ptr(const fs_ensemble *ens, const uint32_t **out);
 
 /* Stream k host rasters (uint8, `pixels` bytes each) through the variant's event
@@ -135,6 +136,10 @@ int fs_ensemble_kernel_ms(fs_ensemble *ens, int kind, float *ms);
 /* The ensemble's compute stream (cudaStream_t) so callers can order collectives and
  * timing events after its work when device_outputs is used.                      */
 int fs_ensemble_stream_handle(fs_ensemble *ens, void **stream);
+/* Run the ensemble's compute work on a caller-owned stream (e.g. the framework's
+ * current stream); NULL restores the ensemble's own stream.  The caller keeps
+ * ownership and must keep the stream alive while the ensemble uses it.           */
+int fs_ensemble_set_stream(fs_ensemble *ens, void *stream);
 /* Blocks until all work queued on the ensemble's streams has finished. */
 int fs_ensemble_sync(fs_ensemble *ens);
 /* Choose the Gram engine used by FS_GRAM_AUTO (process-wide). */

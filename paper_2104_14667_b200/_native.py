@@ -76,6 +76,7 @@ _SIGNATURES = {
     "fs_ensemble_kernel_ms": [_vp, C.c_int, C.POINTER(C.c_float)],
     "fs_ensemble_stream_handle": [_vp, C.POINTER(_vp)],
     "fs_ensemble_sync": [_vp],
+    "fs_ensemble_set_stream": [_vp, _vp],
     "fs_set_gram_engine": [C.c_int],
     "fs_set_pack_engine": [C.c_int],
     "fs_host_alloc": [C.c_uint64, C.POINTER(_vp)],

@@ -404,9 +404,10 @@ struct fs_ensemble {
   DevBuf run_counts;           // running grid of with_kernel streaming
   DevBuf dstage[2];            // device staging slots (raw uint8)
   HostBuf hstage[2];           // pinned staging (initial variants)
-  DevBuf slots, bins, counts, rgba, gram, ws, lut;
+  DevBuf slots, bins, counts, rgba, gram, ws, lut, gather;
   uint64_t lut_n = UINT64_MAX;
   cudaStream_t sc = nullptr, sk = nullptr;
+  cudaStream_t sk_own = nullptr;  // the ensemble's own compute stream
   cudaEvent_t kev[3][2] = {};  // per kernel family: start/end
   bool kev_valid[3] = {false, false, false};
   std::vector<cudaEvent_t> pool;  // timing events for streaming
@@ -472,7 +473,8 @@ int fs_ensemble_create(uint64_t pixels, uint32_t capacity, fs_ensemble **out) {
   CK(cudaMalloc(&e->packed, (size_t)capacity * e->wpm * 4));
   CK(cudaMemset(e->packed, 0, (size_t)capacity * e->wpm * 4));
   CK(cudaStreamCreateWithFlags(&e->sc, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&e->sk, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&e->sk_own, cudaStreamNonBlocking));
+  e->sk = e->sk_own;
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 2; ++j) CK(cudaEventCreate(&e->kev[i][j]));
   *out = e.release();
@@ -486,6 +488,7 @@ int fs_ensemble_destroy(fs_ensemble *e) {
     DeviceGuard dg(e->device);
     cudaStreamSynchronize(e->sc);
     cudaStreamSynchronize(e->sk);
+    cudaStreamSynchronize(e->sk_own);
     cudaFree(e->packed);
     e->run_counts.release();
     for (auto &b : e->dstage) b.release();
@@ -497,11 +500,12 @@ int fs_ensemble_destroy(fs_ensemble *e) {
     e->gram.release();
     e->ws.release();
     e->lut.release();
+    e->gather.release();
     for (auto ev : e->pool) cudaEventDestroy(ev);
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 2; ++j) cudaEventDestroy(e->kev[i][j]);
     cudaStreamDestroy(e->sc);
-    cudaStreamDestroy(e->sk);
+    cudaStreamDestroy(e->sk_own);
   }
   delete e;
   return FS_OK;
@@ -526,6 +530,23 @@ int fs_ensemble_packed_ptr(const fs_ensemble *e, const uint32_t **out) {
 int fs_ensemble_stream_handle(fs_ensemble *e, void **stream) {
   if (!e || !stream) return set_err(FS_EINVAL, "null argument");
   *stream = (void *)e->sk;
+  return FS_OK;
+}
+
+int fs_ensemble_set_stream(fs_ensemble *e, void *stream) {
+  if (!e) return set_err(FS_EINVAL, "null ensemble");
+  std::lock_guard<std::mutex> g(e->mu);
+  DeviceGuard dg(e->device);
+  // order: everything queued so far on the old stream precedes work on the new one
+  cudaStream_t next = stream ? (cudaStream_t)stream : e->sk_own;
+  if (next != e->sk) {
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, e->sk));
+    CK(cudaStreamWaitEvent(next, ev, 0));
+    CK(cudaEventDestroy(ev));
+    e->sk = next;
+  }
   return FS_OK;
 }
 
@@ -606,14 +627,16 @@ int fs_ensemble_stream(fs_ensemble *e, uint32_t first, uint32_t slot_wrap,
     CK(cudaStreamWaitEvent(e->sk, EV(i, 1), 0));
     CK(cudaEventRecord(EV(i, 2), e->sk));
     CK(cudaEventRecord(e->kev[FS_KERNEL_PACK][0], e->sk));
-    uint32_t *dst_slot = e->packed + (size_t)(first + (slot_wrap ? i % slot_wrap : i)) * e->wpm;
-    CK(launch_pack(e->dstage[s].as<uint8_t>(), P, dst_slot, e->wpm, e->sk, -1));
+    const uint64_t dst_slot = first + (slot_wrap ? i % slot_wrap : i);
+    CK(launch_pack(e->dstage[s].as<uint8_t>(), P, e->packed, dst_slot, e->capacity, e->wpm,
+                   e->sk, -1));
     CK(cudaEventRecord(e->kev[FS_KERNEL_PACK][1], e->sk));
     e->kev_valid[FS_KERNEL_PACK] = true;
     CK(cudaEventRecord(EV(i, 3), e->sk));
     if (with_kernel) {
       CK(cudaEventRecord(EV(i, 4), e->sk));
-      CK(launch_accumulate_packed(dst_slot, P, e->run_counts.as<uint32_t>(), e->sk));
+      CK(launch_accumulate_packed(e->packed, dst_slot, e->capacity, P,
+                                  e->run_counts.as<uint32_t>(), e->sk));
       CK(cudaEventRecord(EV(i, 5), e->sk));
     }
   }
@@ -658,8 +681,8 @@ int fs_ensemble_synth(fs_ensemble *e, uint32_t first, uint32_t k, uint64_t seed,
   double t = eps * 4294967296.0;
   sp.flip_thr = t <= 0 ? 0u : (t >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)t);
   for (uint32_t i = 0; i < k; ++i)
-    CK(launch_synth_packed(e->packed + (size_t)(first + i) * e->wpm, e->wpm, sp, mask_index0 + i,
-                           row0, e->pixels, e->sk));
+    CK(launch_synth_packed(e->packed, first + i, e->capacity, e->wpm, sp, mask_index0 + i, row0,
+                           e->pixels, e->sk));
   CK(cudaStreamSynchronize(e->sk));
   return FS_OK;
 }
@@ -680,8 +703,10 @@ int fs_ensemble_overlap(fs_ensemble *e, const uint32_t *slots, uint32_t k, uint6
   const uint64_t P = e->pixels, nbins = n_inputs + 1;
   OverlapArgs a{};
   a.packed = e->packed;
+  a.capacity = e->capacity;
   a.wpm = e->wpm;
   a.slots = e->slots.as<uint32_t>();
+  a.host_slots = slots;
   // first `remainder` slots count cycles+1 times, the rest `cycles` times
   a.k1 = remainder;
   a.w1 = (uint32_t)(cycles + 1);
@@ -795,11 +820,16 @@ int fs_ensemble_gram(fs_ensemble *e, const uint32_t *slots, uint32_t k, int engi
   if (rc) return rc;
   if (engine == FS_GRAM_POPC) {
     CK(cudaMemsetAsync(gd, 0, gbytes, e->sk));
-    CK(launch_gram_popc(e->packed, e->wpm, e->slots.as<uint32_t>(), k, gd, e->sk));
+    CK(launch_gram_popc(e->packed, e->capacity, e->wpm, e->slots.as<uint32_t>(), k, gd, e->sk));
   } else {
     CK(e->ws.ensure(gram_tc_workspace_bytes(k, e->wpm, e->num_sms)));
-    CK(launch_gram_tc(e->packed, e->wpm, e->slots.as<uint32_t>(), k, gd, e->ws.p, e->num_sms,
-                      e->sk));
+    void *gws = nullptr;
+    if (contiguous_run(slots, k) < 0) {
+      CK(e->gather.ensure(gram_tc_gather_bytes(k, e->wpm)));
+      gws = e->gather.p;
+    }
+    CK(launch_gram_tc(e->packed, e->capacity, e->wpm, e->slots.as<uint32_t>(), slots, k, gd,
+                      e->ws.p, gws, e->num_sms, e->sk));
   }
   rc = record_kernel(e, FS_KERNEL_GRAM, false);
   if (rc) return rc;

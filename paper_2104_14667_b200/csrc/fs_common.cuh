@@ -1,12 +1,18 @@
 // fs_common.cuh — shared definitions for libfloodstream (sm_100a).
 //
-// Packed-mask layout in HBM (the "transformed" layout every kernel consumes):
-//   packed[slot][w], w < words_per_mask, uint32, pixel p = 32*w + b stored in bit b
-//   (LSB first).  Pixels are in the raster's flat row-major order, so a row band
-//   [y0, y1) of a mask is the contiguous pixel range [y0*W, y1*W).  words_per_mask
-//   is rounded up to FS_WORD_ALIGN words (1024 px, 128 B) and the padding is zero,
-//   which keeps every per-mask row 128-B aligned for vector loads and lets the
-//   Gram kernels step K in whole 128-px stages without tail handling.
+// Packed-mask layout in HBM (the "transformed", block-tiled layout every kernel
+// consumes).  A mask's pixels (flat row-major raster order, so a row band [y0, y1)
+// is the contiguous pixel range [y0*W, y1*W)) are bit-packed LSB first: pixel
+// p = 32*w + b is bit b of word w.  Words are grouped in TILES of 32 words
+// (1024 px, 128 B) and the tiles of all masks are interleaved:
+//
+//     packed[tile][slot][32 words]        word w of slot s at pk_off(s, w, capacity)
+//
+// so the same K-range (pixel tile) of every mask in the ensemble is ONE contiguous
+// block of capacity x 128 B.  Every consumer streams whole contiguous blocks —
+// the overlap pass reads [tile-group][16 masks][32 words] boxes, the Gram reads
+// [tile][256 masks][32 words] boxes — through 3-D TMA tensor maps (dims: word,
+// slot, tile).  words_per_mask is rounded up to whole tiles; padding is zero.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -18,6 +24,11 @@ namespace fs {
 __host__ __device__ __forceinline__ uint64_t words_for_pixels(uint64_t pixels) {
   uint64_t w = (pixels + 31) / 32;
   return (w + FS_WORD_ALIGN - 1) / FS_WORD_ALIGN * FS_WORD_ALIGN;
+}
+
+// word w of slot s in the tile-interleaved layout
+__host__ __device__ __forceinline__ uint64_t pk_off(uint64_t slot, uint64_t w, uint64_t capacity) {
+  return ((w >> 5) * capacity + slot) * 32u + (w & 31u);
 }
 
 // ---- synthetic flood-like masks (counter based; identical on host and device) ----
@@ -130,6 +141,19 @@ __device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gmem_src, u
           "r"(smem_u32(smem_dst)),
       "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// 3-D TMA tile load (coordinates: word, slot, tile) completing on an mbarrier.
+__device__ __forceinline__ void tma_load_3d(void *smem_dst, const void *tmap, int c0, int c1,
+                                            int c2, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const void *tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {

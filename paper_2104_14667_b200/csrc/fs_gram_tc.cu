@@ -4,13 +4,17 @@
 // (analytics.py:174-181, _kernels_np.py:26-32): |A & B| over wet masks.  Stacking the
 // binarized masks as X (k x P, 0/1) gives I = X X^T, a dense contraction over pixels.
 //
-// Engine: tcgen05.mma.cta_group::1.kind::i8 (u8 x u8 -> s32 in TMEM).
-//  * Masks stay bit-packed in HBM (P/8 bytes each).  Producer warps load 16 B (128 px)
-//    per mask row per stage and expand bits to 0/1 bytes directly into the canonical
-//    K-major SWIZZLE_128B shared-memory layout (one 128-B swizzle row per mask).
-//  * Masks are tiled in panels of PANEL (128 or 256) rows.  A diagonal tile (I == I)
-//    uses ONE smem panel as both the A and the B operand, so every mask row is
-//    expanded once per K step; the MMA reads it as M rows and as N columns.
+// Engine: tcgen05.mma.cta_group::1.kind::i8 (u8 x u8 -> s32 accumulators in TMEM).
+//  * Masks stay bit-packed in HBM (P/8 bytes each) in the tile-interleaved layout, so
+//    one pixel tile of a whole 256-mask panel is a single contiguous 32 KB block.  A
+//    TMA warp streams those blocks (3-D tensor map, SWIZZLE_128B/64B) into a raw SMEM
+//    ring; expander warps turn each 128-px slice of every row into 0/1 bytes written
+//    straight into the canonical K-major SWIZZLE_128B operand layout (one 128-B row
+//    per mask); one elected thread issues the MMAs.  Both SMEM reads of the expanders
+//    (swizzled raw) and their writes (swizzled operand) are bank-conflict free.
+//  * Masks are tiled in panels of PANEL (128 or 256) rows.  A diagonal tile (I == J)
+//    uses ONE operand panel as both A and B: every mask row is expanded once per K
+//    step and read by the MMA as M rows and as N columns.
 //  * PANEL = 256: two M=128 halves.  Diagonal tiles issue half 0 with N=256 and half 1
 //    with N=128 (columns 128..255) — the lower-left quadrant is the transpose of the
 //    upper-right one and is mirrored by the reduce kernel (3/4 of the full work).
@@ -25,26 +29,26 @@ namespace fs {
 
 namespace tc {
 
-constexpr int kThreads = 160;  // warp 0: TMEM alloc + MMA issue; warps 1..4: producers/epilogue
-constexpr int kStagePx = 128;  // K per stage: one 128-B SW128 row per mask
+constexpr int kThreads = 192;  // w0: TMEM alloc + MMA; w1..4: expanders + epilogue; w5: TMA
+constexpr int kStagePx = 128;  // K per operand stage: one 128-B SW128 row per mask
 constexpr int kSmemBudget = 200 * 1024;
-constexpr int kPrefetch = 4;   // producer register prefetch depth (stages)
+constexpr int kRawDepth = 2;
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
   uint64_t d = 0;
-  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);   // start address
-  d |= (uint64_t)1u << 16;                       // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024u >> 4) << 32;             // SBO: 8 rows x 128 B
-  d |= (uint64_t)1u << 46;                       // descriptor version (sm_100)
-  d |= (uint64_t)2u << 61;                       // SWIZZLE_128B
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);  // start address
+  d |= (uint64_t)1u << 16;                      // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;            // SBO: 8 rows x 128 B
+  d |= (uint64_t)1u << 46;                      // descriptor version (sm_100)
+  d |= (uint64_t)2u << 61;                      // SWIZZLE_128B
   return d;
 }
 
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
-  return (2u << 4)                       // D format: S32
-         | (0u << 7) | (0u << 10)        // A, B: unsigned 8-bit
-         | ((uint32_t)(N >> 3) << 17)    // N
-         | ((uint32_t)(M >> 4) << 24);   // M
+  return (2u << 4)                      // D format: S32
+         | (0u << 7) | (0u << 10)       // A, B: unsigned 8-bit
+         | ((uint32_t)(N >> 3) << 17)   // N
+         | ((uint32_t)(M >> 4) << 24);  // M
 }
 
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
@@ -83,7 +87,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// 16 bits -> 16 bytes of 0/1, written as one swizzled 16-B chunk
+// 16 bits -> 16 bytes of 0/1
 __device__ __forceinline__ uint4 expand16(uint32_t half) {
   uint4 o;
   o.x = ((half & 0xFu) * 0x00204081u) & 0x01010101u;
@@ -98,8 +102,16 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
                "r"(v.z), "r"(v.w)
                : "memory");
 }
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
 
-// Expand one 128-px row (4 words) into the SW128 row `row` of a panel at `base`.
+// Expand one 128-px row slice (4 words) into SW128 operand row `row` at `base`.
 __device__ __forceinline__ void expand_row(uint32_t base, uint32_t row, uint4 v) {
   const uint32_t rbase = base + row * 128u;
   const uint32_t sw = row & 7u;
@@ -113,30 +125,40 @@ __device__ __forceinline__ void expand_row(uint32_t base, uint32_t row, uint4 v)
 
 template <int PANEL, bool DIAG>
 struct Cfg {
-  static constexpr int kRowsPerThread = PANEL / 128;        // per region
+  static constexpr int kRowsPerThread = PANEL / 128;  // per region, 128 expander threads
   static constexpr int kRegions = DIAG ? 1 : 2;
+  static constexpr int kRawRow = (PANEL == 256 && !DIAG) ? 64 : 128;  // raw bytes/row/unit
+  static constexpr int kStagesPerUnit = kRawRow / 16;
+  static constexpr int kRawUnitBytes = kRegions * PANEL * kRawRow;
   static constexpr int kRegionBytes = PANEL * 128;
   static constexpr int kStageBytes = kRegionBytes * kRegions;
-  static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
+  static constexpr int kStagesFit = (kSmemBudget - kRawDepth * kRawUnitBytes) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   static constexpr int kHalves = PANEL / 128;
   static constexpr uint32_t kTmemCols = PANEL == 256 ? 512u : 128u;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes =
+      kRawDepth * kRawUnitBytes + kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(kStages >= 2, "operand ring too shallow");
 };
 
 template <int PANEL, bool DIAG>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gram_tc(const uint32_t *__restrict__ packed, uint64_t wpm, const uint32_t *__restrict__ slots,
-              uint32_t k, uint32_t npanels, uint32_t kchunks, uint64_t stages_per_chunk,
-              uint64_t total_stages, int32_t *__restrict__ partial) {
+    k_gram_tc(const __grid_constant__ CUtensorMap tm, uint32_t npanels, uint32_t kchunks,
+              uint64_t units_per_chunk, uint64_t total_units, int32_t *__restrict__ partial) {
   using C = Cfg<PANEL, DIAG>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   const uint32_t pad = (1024u - (raw_addr & 1023u)) & 1023u;
   uint8_t *smem = smem_raw + pad;
   const uint32_t smem_base = raw_addr + pad;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);
+  const uint32_t raw_base = smem_base;                                  // raw ring
+  const uint32_t op_base = smem_base + kRawDepth * C::kRawUnitBytes;    // operand stages
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kRawDepth * C::kRawUnitBytes +
+                                                C::kStages * C::kStageBytes);
   uint64_t *empty = full + C::kStages;
-  uint64_t *tmem_full = empty + C::kStages;
+  uint64_t *raw_full = empty + C::kStages;
+  uint64_t *raw_empty = raw_full + kRawDepth;
+  uint64_t *tmem_full = raw_empty + kRawDepth;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
   const int tid = threadIdx.x;
@@ -157,14 +179,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     J = I + 1 + t;
   }
-  const uint64_t st0 = (uint64_t)kc * stages_per_chunk;
-  const uint64_t st1 = min(st0 + stages_per_chunk, total_stages);
-  const int nst = st1 > st0 ? (int)(st1 - st0) : 0;
+  const uint64_t u0 = (uint64_t)kc * units_per_chunk;
+  const uint64_t u1 = min(u0 + units_per_chunk, total_units);
+  const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
+  const int nst = nunits * C::kStagesPerUnit;
 
   if (tid == 0) {
+    ptx::prefetch_tmap(&tm);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&full[s], 128);
       ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kRawDepth; ++s) {
+      ptx::mbar_init(&raw_full[s], 1);
+      ptx::mbar_init(&raw_empty[s], 128);
     }
     ptx::mbar_init(tmem_full, 1);
     ptx::fence_mbar_init();
@@ -189,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = j % C::kStages;
         ptx::mbar_wait(&full[s], (uint32_t)((j / C::kStages) & 1));
         fence_after();
-        const uint32_t a_base = smem_base + s * C::kStageBytes;
+        const uint32_t a_base = op_base + s * C::kStageBytes;
         const uint32_t b_base = DIAG ? a_base : a_base + C::kRegionBytes;
 #pragma unroll
         for (int ks = 0; ks < kStagePx / 32; ++ks) {
@@ -212,50 +240,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit(tmem_full);
     }
     __syncwarp();
-  } else {
-    // ===== producers: bits -> 0/1 bytes in SW128 K-major smem =====
-    const uint32_t ptid = (uint32_t)(tid - 32);
-    const uint32_t *rowp[C::kRegions][C::kRowsPerThread];
+  } else if (warp == 5) {
+    // ===== TMA loader: one contiguous [PANEL rows][raw row] box per region per unit =====
+    if (lane == 0) {
+      constexpr int kUnitsPerTile = 128 / C::kRawRow;
+      for (int u = 0; u < nunits; ++u) {
+        const int ru = u % kRawDepth;
+        if (u >= kRawDepth) ptx::mbar_wait(&raw_empty[ru], (uint32_t)(((u / kRawDepth) - 1) & 1));
+        const uint64_t gu = u0 + (uint64_t)u;
+        const int c0 = (int)(gu % kUnitsPerTile) * (C::kRawRow / 4);
+        const int c2 = (int)(gu / kUnitsPerTile);
+        ptx::mbar_arrive_expect_tx(&raw_full[ru], C::kRawUnitBytes);
 #pragma unroll
-    for (int r = 0; r < C::kRegions; ++r)
-#pragma unroll
-      for (int m = 0; m < C::kRowsPerThread; ++m) {
-        const uint32_t panel = (r == 0) ? I : J;
-        const uint32_t row = panel * PANEL + ptid + m * 128;
-        rowp[r][m] = row < k ? packed + (uint64_t)__ldg(slots + row) * wpm : nullptr;
+        for (int r = 0; r < C::kRegions; ++r) {
+          const uint32_t panel = r == 0 ? I : J;
+          ptx::tma_load_3d(smem + ru * C::kRawUnitBytes + r * PANEL * C::kRawRow, &tm, c0,
+                           (int)(panel * PANEL), c2, &raw_full[ru]);
+        }
       }
-    uint4 buf[kPrefetch][C::kRegions][C::kRowsPerThread];
-    auto load_stage = [&](int j, uint4 (&dst)[C::kRegions][C::kRowsPerThread]) {
+    }
+    __syncwarp();
+  } else {
+    // ===== expanders: raw bits (swizzled) -> 0/1 bytes in SW128 K-major operand =====
+    const uint32_t ptid = (uint32_t)(tid - 32);
+    for (int j = 0; j < nst; ++j) {
+      const int u = j / C::kStagesPerUnit;
+      const int sub = j % C::kStagesPerUnit;
+      const int ru = u % kRawDepth;
+      const int s = j % C::kStages;
+      if (sub == 0) ptx::mbar_wait(&raw_full[ru], (uint32_t)((u / kRawDepth) & 1));
+      if (j >= C::kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / C::kStages) - 1) & 1));
+      const uint32_t sbase = op_base + s * C::kStageBytes;
+      const uint32_t rbase = raw_base + ru * C::kRawUnitBytes;
 #pragma unroll
       for (int r = 0; r < C::kRegions; ++r)
 #pragma unroll
         for (int m = 0; m < C::kRowsPerThread; ++m) {
-          uint4 v = make_uint4(0, 0, 0, 0);
-          if (j < nst && rowp[r][m] != nullptr)
-            v = ptx::ld_nc_v4(rowp[r][m] + (st0 + (uint64_t)j) * (kStagePx / 32));
-          dst[r][m] = v;
+          const uint32_t rr = ptid + m * 128;
+          const uint32_t sw = C::kRawRow == 128 ? (rr & 7u) : ((rr >> 1) & 3u);
+          const uint4 v = ld_shared_v4(rbase + r * PANEL * C::kRawRow + rr * C::kRawRow +
+                                       (((uint32_t)sub ^ sw) << 4));
+          expand_row(sbase + r * C::kRegionBytes, rr, v);
         }
-    };
-#pragma unroll
-    for (int d = 0; d < kPrefetch; ++d) load_stage(d, buf[d]);
-    for (int j0 = 0; j0 < nst; j0 += kPrefetch) {
-#pragma unroll
-      for (int d = 0; d < kPrefetch; ++d) {
-        const int j = j0 + d;
-        if (j < nst) {
-          const int s = j % C::kStages;
-          if (j >= C::kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / C::kStages) - 1) & 1));
-          const uint32_t sbase = smem_base + s * C::kStageBytes;
-#pragma unroll
-          for (int r = 0; r < C::kRegions; ++r)
-#pragma unroll
-            for (int m = 0; m < C::kRowsPerThread; ++m)
-              expand_row(sbase + r * C::kRegionBytes, ptid + m * 128, buf[d][r][m]);
-          ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(&full[s]);
-          load_stage(j + kPrefetch, buf[d]);
-        }
-      }
+      ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive(&full[s]);
+      if (sub == C::kStagesPerUnit - 1) ptx::mbar_arrive(&raw_empty[ru]);
     }
     // ===== epilogue: TMEM -> registers -> int32 partial tile =====
     const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp
@@ -271,7 +300,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c_begin = lower_diag ? 128 : 0;
       for (int c0 = c_begin; c0 < PANEL; c0 += 32) {
         uint32_t v[32];
-        const uint32_t col = lower_diag ? (256u + (uint32_t)(c0 - 128)) : (uint32_t)(h * PANEL + c0);
+        const uint32_t col =
+            lower_diag ? (256u + (uint32_t)(c0 - 128)) : (uint32_t)(h * PANEL + c0);
         tmem_ld32(tmem + ((q * 32u) << 16) + col, v);
         if (nst == 0) {
 #pragma unroll
@@ -338,26 +368,40 @@ __global__ void k_gram_reduce(const int32_t *__restrict__ part_diag, uint32_t kc
   }
 }
 
+// Gather arbitrary slots into a contiguous tile-interleaved copy (rows 0..k-1).
+__global__ void k_gather_slots(const uint32_t *__restrict__ packed, uint64_t cap,
+                               const uint32_t *__restrict__ slots, uint32_t k, uint64_t ntiles,
+                               uint32_t *__restrict__ dst) {
+  const uint64_t total = ntiles * k * 8;  // uint4 per (tile, row): 8
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = e / ((uint64_t)k * 8);
+    const uint32_t i = (uint32_t)((e / 8) % k), v = (uint32_t)(e % 8);
+    const uint4 *src = reinterpret_cast<const uint4 *>(packed + (t * cap + slots[i]) * 32) + v;
+    reinterpret_cast<uint4 *>(dst + (t * k + i) * 32)[v] = *src;
+  }
+}
+
 struct Plan {
   int panel;
   uint32_t npanels, ndiag, noff;
-  uint64_t total_stages;
+  uint64_t units_diag, units_off;  // raw units along K for each tile kind
   uint32_t kc_diag, kc_off;
-  uint64_t spc_diag, spc_off;
+  uint64_t upc_diag, upc_off;
 };
 
-static void chunking(uint64_t total_stages, uint32_t ntiles, int num_sms, uint32_t &kc,
-                     uint64_t &spc) {
-  if (ntiles == 0) {
+static void chunking(uint64_t total_units, uint32_t ntiles, int num_sms, uint32_t &kc,
+                     uint64_t &upc) {
+  if (ntiles == 0 || total_units == 0) {
     kc = 0;
-    spc = 0;
+    upc = 0;
     return;
   }
   uint64_t want = ((uint64_t)num_sms + ntiles - 1) / ntiles;
   if (want < 1) want = 1;
-  if (want > total_stages) want = total_stages;
-  spc = (total_stages + want - 1) / want;
-  kc = (uint32_t)((total_stages + spc - 1) / spc);
+  if (want > total_units) want = total_units;
+  upc = (total_units + want - 1) / want;
+  kc = (uint32_t)((total_units + upc - 1) / upc);
 }
 
 static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms) {
@@ -366,9 +410,11 @@ static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms) {
   p.npanels = (k + p.panel - 1) / p.panel;
   p.ndiag = p.npanels;
   p.noff = p.npanels * (p.npanels - 1) / 2;
-  p.total_stages = wpm / (kStagePx / 32);
-  chunking(p.total_stages, p.ndiag, num_sms, p.kc_diag, p.spc_diag);
-  chunking(p.total_stages, p.noff, num_sms, p.kc_off, p.spc_off);
+  const uint64_t ntiles = wpm / 32;
+  p.units_diag = ntiles;  // diag tiles: one 128-B raw row per tile
+  p.units_off = p.panel == 256 ? ntiles * 2 : ntiles;  // 256-panel off-diag: 64-B halves
+  chunking(p.units_diag, p.ndiag, num_sms, p.kc_diag, p.upc_diag);
+  chunking(p.units_off, p.noff, num_sms, p.kc_off, p.upc_off);
   return p;
 }
 
@@ -381,12 +427,13 @@ size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms) {
 }
 
 template <int PANEL, bool DIAG>
-static cudaError_t launch_one(const uint32_t *packed, uint64_t wpm, const uint32_t *slots,
-                              uint32_t k, const tc::Plan &p, int32_t *part, cudaStream_t s) {
+static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t *part,
+                              cudaStream_t s) {
   using C = tc::Cfg<PANEL, DIAG>;
   const uint32_t ntiles = DIAG ? p.ndiag : p.noff;
   const uint32_t kc = DIAG ? p.kc_diag : p.kc_off;
-  const uint64_t spc = DIAG ? p.spc_diag : p.spc_off;
+  const uint64_t upc = DIAG ? p.upc_diag : p.upc_off;
+  const uint64_t units = DIAG ? p.units_diag : p.units_off;
   if (ntiles == 0 || kc == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -397,29 +444,55 @@ static cudaError_t launch_one(const uint32_t *packed, uint64_t wpm, const uint32
     attr = true;
   }
   tc::k_gram_tc<PANEL, DIAG><<<ntiles * kc, tc::kThreads, C::kSmemBytes, s>>>(
-      packed, wpm, slots, k, p.npanels, kc, spc, p.total_stages, part);
+      tm, p.npanels, kc, upc, units, part);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t wpm, const uint32_t *slots, uint32_t k,
-                           unsigned long long *gram, void *workspace, int num_sms,
-                           cudaStream_t s) {
+size_t gram_tc_gather_bytes(uint32_t k, uint64_t wpm) { return (size_t)k * wpm * 4; }
+
+cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t wpm,
+                           const uint32_t *slots, const uint32_t *host_slots, uint32_t k,
+                           unsigned long long *gram, void *workspace, void *gather_ws,
+                           int num_sms, cudaStream_t s) {
   if (k == 0) return cudaSuccess;
   tc::Plan p = tc::make_plan(k, wpm, num_sms);
+  const uint64_t ntiles = wpm / 32;
+  // contiguous slot run -> map straight over the ensemble; else gather first
+  const uint32_t *src = packed;
+  uint64_t src_cap = capacity, row0 = 0;
+  const int64_t first = contiguous_run(host_slots, k);
+  cudaError_t e;
+  if (first >= 0) {
+    row0 = (uint64_t)first;
+  } else {
+    if (gather_ws == nullptr) return cudaErrorInvalidValue;
+    uint64_t total = ntiles * k * 8;
+    uint64_t grid = (total + 255) / 256;
+    if (grid > (uint64_t)num_sms * 16) grid = (uint64_t)num_sms * 16;
+    tc::k_gather_slots<<<(unsigned)grid, 256, 0, s>>>(packed, capacity, slots, k, ntiles,
+                                                      static_cast<uint32_t *>(gather_ws));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    src = static_cast<const uint32_t *>(gather_ws);
+    src_cap = k;
+  }
   const uint64_t per_tile = (uint64_t)p.panel * p.panel;
   int32_t *part_diag = reinterpret_cast<int32_t *>(workspace);
   int32_t *part_off = part_diag + (uint64_t)p.ndiag * p.kc_diag * per_tile;
-  cudaError_t e;
+  CUtensorMap tm_diag, tm_off;
+  const uint32_t raw_off = p.panel == 256 ? 16u : 32u;  // box words for off-diag units
+  if ((e = encode_packed_map(&tm_diag, src, src_cap, row0, k, ntiles, 32, p.panel, 1, 128)) !=
+      cudaSuccess)
+    return e;
+  if ((e = encode_packed_map(&tm_off, src, src_cap, row0, k, ntiles, raw_off, p.panel, 1,
+                             raw_off == 16 ? 64 : 128)) != cudaSuccess)
+    return e;
   if (p.panel == 128) {
-    e = launch_one<128, true>(packed, wpm, slots, k, p, part_diag, s);
-    if (e != cudaSuccess) return e;
-    e = launch_one<128, false>(packed, wpm, slots, k, p, part_off, s);
+    if ((e = launch_one<128, true>(tm_diag, p, part_diag, s)) != cudaSuccess) return e;
+    if ((e = launch_one<128, false>(tm_off, p, part_off, s)) != cudaSuccess) return e;
   } else {
-    e = launch_one<256, true>(packed, wpm, slots, k, p, part_diag, s);
-    if (e != cudaSuccess) return e;
-    e = launch_one<256, false>(packed, wpm, slots, k, p, part_off, s);
+    if ((e = launch_one<256, true>(tm_diag, p, part_diag, s)) != cudaSuccess) return e;
+    if ((e = launch_one<256, false>(tm_off, p, part_off, s)) != cudaSuccess) return e;
   }
-  if (e != cudaSuccess) return e;
   const uint64_t total = (uint64_t)(p.ndiag + p.noff) * per_tile;
   uint64_t grid = (total + 255) / 256;
   if (grid > (uint64_t)num_sms * 8) grid = (uint64_t)num_sms * 8;

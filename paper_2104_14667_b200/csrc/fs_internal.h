@@ -1,20 +1,34 @@
 // fs_internal.h — launchers shared between the kernel files and the C ABI layer.
 #pragma once
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (types only; the encoder is fetched at run time)
 #include <cuda_runtime.h>
 
 #include "fs_common.cuh"
 
 namespace fs {
 
-constexpr uint32_t kHistSmemBins = 4096;   // overlap classes kept in shared memory
+constexpr uint32_t kHistSmemBins = 4096;       // overlap classes kept in shared memory
 constexpr uint64_t kLutMaxEntries = 1u << 20;  // composite grey LUT (n_inputs + 1)
 
+int num_sms();
+
+// 3-D tensor map over the tile-interleaved packed layout, restricted to rows
+// [row0, row0 + rows) of `capacity`: dims (32 words, rows, ntiles), box
+// (box_words, box_rows, box_tiles), swizzle 0 / 64 / 128 (bytes).  Rows and tiles
+// outside the map read as zero.
+cudaError_t encode_packed_map(CUtensorMap *out, const uint32_t *packed, uint64_t capacity,
+                              uint64_t row0, uint64_t rows, uint64_t ntiles, uint32_t box_words,
+                              uint32_t box_rows, uint32_t box_tiles, int swizzle);
+
+// Slot list -> first slot if it is a contiguous ascending run, else -1.
+int64_t contiguous_run(const uint32_t *host_slots, uint32_t k);
+
 // ---- transform ---------------------------------------------------------------
-// Binarize + bit-pack one raster of `pixels` bytes into `words_per_mask` words
-// (zero padded).  engine 0 = TMA bulk-staged (default), 1 = direct vector loads.
-cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint64_t wpm,
-                        cudaStream_t s, int engine);
+// Binarize + bit-pack one raster of `pixels` bytes into slot `slot` of the packed
+// buffer (zero padded to wpm words).  engine 0 = TMA bulk-staged, 1 = direct loads.
+cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *packed, uint64_t slot,
+                        uint64_t capacity, uint64_t wpm, cudaStream_t s, int engine);
 void set_pack_engine(int engine);
 int get_pack_engine();
 
@@ -31,9 +45,11 @@ cudaError_t launch_pair_counts(const uint8_t *a, const uint8_t *b, uint64_t n,
 // ---- packed-ensemble kernels -------------------------------------------------
 struct OverlapArgs {
   const uint32_t *packed;
+  uint64_t capacity;
   uint64_t wpm;
-  const uint32_t *slots;  // device slot list: [k1 | k2]
-  uint32_t k1, k2;        // the first k1 slots count with weight w1, the next k2 with w2
+  const uint32_t *slots;      // device slot list [k1 | k2] (gather mode)
+  const uint32_t *host_slots; // same list on the host (mode selection)
+  uint32_t k1, k2;            // first k1 slots count with weight w1, next k2 with w2
   uint32_t w1, w2;
   uint64_t pixels;
   uint32_t *counts;           // may be null
@@ -45,23 +61,27 @@ struct OverlapArgs {
 };
 cudaError_t launch_overlap(const OverlapArgs &a, cudaStream_t s);
 
-cudaError_t launch_accumulate_packed(const uint32_t *packed_mask, uint64_t pixels,
-                                     uint32_t *counts, cudaStream_t s);
+cudaError_t launch_accumulate_packed(const uint32_t *packed, uint64_t slot, uint64_t capacity,
+                                     uint64_t pixels, uint32_t *counts, cudaStream_t s);
 
-cudaError_t launch_gram_popc(const uint32_t *packed, uint64_t wpm, const uint32_t *slots,
-                             uint32_t k, unsigned long long *gram, cudaStream_t s);
+cudaError_t launch_gram_popc(const uint32_t *packed, uint64_t capacity, uint64_t wpm,
+                             const uint32_t *slots, uint32_t k, unsigned long long *gram,
+                             cudaStream_t s);
 // tcgen05 kind::i8 Gram; partial workspace sized by gram_tc_workspace_bytes().
 size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms);
-cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t wpm, const uint32_t *slots,
-                           uint32_t k, unsigned long long *gram, void *workspace,
+// Non-contiguous slot lists are first gathered into gather_ws (gram_tc_gather_bytes).
+size_t gram_tc_gather_bytes(uint32_t k, uint64_t wpm);
+cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t wpm,
+                           const uint32_t *slots, const uint32_t *host_slots, uint32_t k,
+                           unsigned long long *gram, void *workspace, void *gather_ws,
                            int num_sms, cudaStream_t s);
-// gram (k x k, upper tiles filled) -> int64 symmetric
+// gram (k x k, upper tiles filled) -> symmetric
 cudaError_t launch_gram_mirror(unsigned long long *gram, uint32_t k, uint32_t tile,
                                cudaStream_t s);
 
-cudaError_t launch_synth_packed(uint32_t *dst, uint64_t wpm, const SynthParams &sp,
-                                uint64_t mask, uint64_t row0, uint64_t pixels,
-                                cudaStream_t s);
+cudaError_t launch_synth_packed(uint32_t *packed, uint64_t slot, uint64_t capacity, uint64_t wpm,
+                                const SynthParams &sp, uint64_t mask, uint64_t row0,
+                                uint64_t pixels, cudaStream_t s);
 
 // Composite grey LUT in FP64, bit-exact with _kernels_np.py:41-42.
 void build_grey_lut(uint64_t n_inputs, uint8_t *lut, uint64_t entries);

@@ -13,12 +13,14 @@
 #include <cstdio>
 #include <cmath>
 
+#include <cudaTypedefs.h>
+
 #include "fs_internal.h"
 
 namespace fs {
 
 static int g_num_sms = 0;
-static int num_sms() {
+int num_sms() {
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -70,7 +72,8 @@ void set_pack_engine(int e) { g_pack_engine = e; }
 int get_pack_engine() { return g_pack_engine; }
 
 __global__ void __launch_bounds__(kPackThreads)
-    k_pack_bulk(const uint8_t *__restrict__ src, uint64_t nchunks, uint32_t *__restrict__ dst) {
+    k_pack_bulk(const uint8_t *__restrict__ src, uint64_t nchunks, uint32_t *__restrict__ dst,
+                uint64_t slot, uint64_t cap) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(sm + kPackStages * kPackChunk);
   const int tid = threadIdx.x;
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(kPackThreads)
       const int q = tid + i * kPackThreads;
       uint32_t h = nz_bits16(stage[q]);
       uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
-      if ((lane & 1) == 0) dst[c * (kPackChunk / 32) + (q >> 1)] = h | (other << 16);
+      if ((lane & 1) == 0) dst[pk_off(slot, c * (kPackChunk / 32) + (q >> 1), cap)] = h | (other << 16);
     }
     __syncthreads();
     if (tid == 0 && j + kPackStages < nmy) {
@@ -113,7 +116,8 @@ __global__ void __launch_bounds__(kPackThreads)
 
 // Direct-load variant (no staging): each thread turns 32 bytes into one word.
 __global__ void __launch_bounds__(256)
-    k_pack_direct(const uint8_t *__restrict__ src, uint64_t nvec, uint32_t *__restrict__ dst) {
+    k_pack_direct(const uint8_t *__restrict__ src, uint64_t nvec, uint32_t *__restrict__ dst,
+                  uint64_t slot, uint64_t cap) {
   // nvec = number of full 16-byte vectors; pairs of lanes build one word
   const int lane = threadIdx.x & 31;
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -121,13 +125,14 @@ __global__ void __launch_bounds__(256)
     uint32_t h = 0;
     if (q < nvec) h = nz_bits16(ptx::ld_nc_v4(src + q * 16));
     uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
-    if ((lane & 1) == 0 && q < nvec) dst[q >> 1] = h | (other << 16);
+    if ((lane & 1) == 0 && q < nvec) dst[pk_off(slot, q >> 1, cap)] = h | (other << 16);
   }
 }
 
 // Words [w0, wpm): scalar tail + zero padding.
 __global__ void k_pack_tail(const uint8_t *__restrict__ src, uint64_t pixels, uint64_t w0,
-                            uint64_t wpm, uint32_t *__restrict__ dst) {
+                            uint64_t wpm, uint32_t *__restrict__ dst, uint64_t slot,
+                            uint64_t cap) {
   uint64_t w = w0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (w >= wpm) return;
   uint32_t word = 0;
@@ -138,11 +143,11 @@ __global__ void k_pack_tail(const uint8_t *__restrict__ src, uint64_t pixels, ui
       if (p < pixels && src[p] != 0) word |= 1u << b;
     }
   }
-  dst[w] = word;
+  dst[pk_off(slot, w, cap)] = word;
 }
 
-cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint64_t wpm,
-                        cudaStream_t s, int engine) {
+cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint64_t slot,
+                        uint64_t cap, uint64_t wpm, cudaStream_t s, int engine) {
   if (engine < 0) engine = g_pack_engine;
   uint64_t done_words = 0;
   if (engine == 0) {
@@ -156,7 +161,7 @@ cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint
       }
       uint64_t grid = (uint64_t)num_sms() * 6;
       if (grid > nchunks) grid = nchunks;
-      k_pack_bulk<<<(unsigned)grid, kPackThreads, smem, s>>>(src, nchunks, dst);
+      k_pack_bulk<<<(unsigned)grid, kPackThreads, smem, s>>>(src, nchunks, dst, slot, cap);
       done_words = nchunks * (kPackChunk / 32);
     }
   } else {
@@ -165,15 +170,16 @@ cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint
     if (nvec > 0) {
       uint64_t threads = (nvec + 31) / 32 * 32;
       uint64_t grid = (threads + 255) / 256;
-      uint64_t cap = (uint64_t)num_sms() * 16;
-      if (grid > cap) grid = cap;
-      k_pack_direct<<<(unsigned)grid, 256, 0, s>>>(src, nvec, dst);
+      const uint64_t gcap = (uint64_t)num_sms() * 16;
+      if (grid > gcap) grid = gcap;
+      k_pack_direct<<<(unsigned)grid, 256, 0, s>>>(src, nvec, dst, slot, cap);
       done_words = nvec / 2;
     }
   }
   if (done_words < wpm) {
     uint64_t n = wpm - done_words;
-    k_pack_tail<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, pixels, done_words, wpm, dst);
+    k_pack_tail<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, pixels, done_words, wpm, dst,
+                                                            slot, cap);
   }
   return cudaGetLastError();
 }
@@ -338,11 +344,25 @@ cudaError_t launch_pair_counts(const uint8_t *a, const uint8_t *b, uint64_t n,
 }
 
 // ---------------------------------------------------------------------------
-// Fused overlap pass over bit-packed masks: bit-sliced Harley-Seal counters per
-// 32-pixel word, then counts / composite / histogram in one epilogue.
+// Fused overlap pass over the tile-interleaved packed masks.
+//
+// A block owns 4 consecutive pixel tiles (4 warps, warp = tile, lane = word: 32 px).
+// TMA streams [4 tiles][16 masks][32 words] boxes (8 KB, contiguous in HBM) through a
+// 4-stage mbarrier ring; each thread folds its word of 16 masks into bit-sliced
+// Harley-Seal counters (ones/twos/fours/eights + ripple planes), so one 32-bit op
+// advances 32 pixels.  After the last mask the per-pixel counts are extracted,
+// transposed through SMEM and written lane-contiguously as counts / RGBA, and the
+// histogram is accumulated in SMEM with warp-aggregated atomics.
 // ---------------------------------------------------------------------------
-constexpr int kOvThreads = 128;
-constexpr int kOvNH = 12;  // high planes: 16 * (2^12 - 1) + 15 masks per pass
+constexpr int kOvTiles = 4;
+constexpr int kOvThreads = 32 * kOvTiles;
+constexpr int kOvGroup = 16;
+constexpr int kOvStages = 4;
+constexpr int kOvStageWords = kOvTiles * kOvGroup * 32;  // 8 KB
+constexpr int kOvNH = 12;                                 // ripple planes (x16 masks)
+constexpr uint32_t kOvGroupsPerPass = (1u << kOvNH) - 1;
+constexpr size_t kOvSmem = (size_t)kOvStages * kOvStageWords * 4 + kHistSmemBins * 4 +
+                           kOvTiles * 32 * 33 * 4 + kOvStages * 8;
 
 __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b,
                                     uint32_t c) {
@@ -351,105 +371,166 @@ __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32
   l = u ^ c;
 }
 
-// Count one slot range [off, off+k) for word w into cnt[32] with weight `wt`.
-__device__ __forceinline__ void count_range(const uint32_t *__restrict__ packed, uint64_t wpm,
-                                            const uint32_t *__restrict__ slots, uint32_t off,
-                                            uint32_t k, uint64_t w, bool valid, uint32_t wt,
-                                            uint32_t (&cnt)[32]) {
-  constexpr uint32_t kGroupsPerPass = (1u << kOvNH) - 1;
-  for (uint32_t pass0 = 0; pass0 < k; pass0 += kGroupsPerPass * 16) {
-    const uint32_t kp = min(k - pass0, kGroupsPerPass * 16);
-    uint32_t ones = 0, twos = 0, fours = 0, eights = 0;
-    uint32_t H[kOvNH];
+struct HSCounter {
+  uint32_t ones, twos, fours, eights;
+  uint32_t H[kOvNH];
+  __device__ __forceinline__ void reset() {
+    ones = twos = fours = eights = 0;
 #pragma unroll
     for (int i = 0; i < kOvNH; ++i) H[i] = 0;
-    for (uint32_t g = 0; g < kp; g += 16) {
-      uint32_t d[16];
+  }
+  __device__ __forceinline__ void add16(const uint32_t (&d)[16]) {
+    uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
+    csa(twosA, ones, ones, d[0], d[1]);
+    csa(twosB, ones, ones, d[2], d[3]);
+    csa(foursA, twos, twos, twosA, twosB);
+    csa(twosA, ones, ones, d[4], d[5]);
+    csa(twosB, ones, ones, d[6], d[7]);
+    csa(foursB, twos, twos, twosA, twosB);
+    csa(eightsA, fours, fours, foursA, foursB);
+    csa(twosA, ones, ones, d[8], d[9]);
+    csa(twosB, ones, ones, d[10], d[11]);
+    csa(foursA, twos, twos, twosA, twosB);
+    csa(twosA, ones, ones, d[12], d[13]);
+    csa(twosB, ones, ones, d[14], d[15]);
+    csa(foursB, twos, twos, twosA, twosB);
+    csa(eightsB, fours, fours, foursA, foursB);
+    csa(sixteens, eights, eights, eightsA, eightsB);
+    uint32_t carry = sixteens;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        d[j] = 0;
-        if (valid && g + j < kp) {
-          const uint32_t slot = __ldg(slots + off + pass0 + g + j);
-          d[j] = ptx::ld_nc_u32(packed + (uint64_t)slot * wpm + w);
-        }
-      }
-      uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
-      csa(twosA, ones, ones, d[0], d[1]);
-      csa(twosB, ones, ones, d[2], d[3]);
-      csa(foursA, twos, twos, twosA, twosB);
-      csa(twosA, ones, ones, d[4], d[5]);
-      csa(twosB, ones, ones, d[6], d[7]);
-      csa(foursB, twos, twos, twosA, twosB);
-      csa(eightsA, fours, fours, foursA, foursB);
-      csa(twosA, ones, ones, d[8], d[9]);
-      csa(twosB, ones, ones, d[10], d[11]);
-      csa(foursA, twos, twos, twosA, twosB);
-      csa(twosA, ones, ones, d[12], d[13]);
-      csa(twosB, ones, ones, d[14], d[15]);
-      csa(foursB, twos, twos, twosA, twosB);
-      csa(eightsB, fours, fours, foursA, foursB);
-      csa(sixteens, eights, eights, eightsA, eightsB);
-      uint32_t carry = sixteens;
-#pragma unroll
-      for (int i = 0; i < kOvNH; ++i) {
-        const uint32_t t = H[i] & carry;
-        H[i] ^= carry;
-        carry = t;
-      }
+    for (int i = 0; i < kOvNH; ++i) {
+      const uint32_t t = H[i] & carry;
+      H[i] ^= carry;
+      carry = t;
     }
-    // extract: c = ones + 2 twos + 4 fours + 8 eights + 16 * sum_i H[i] 2^i
-    const uint32_t ngroups = (kp + 15) / 16;
+  }
+  // cnt[j] += wt * count(pixel j); ngroups bounds the ripple planes in use
+  __device__ __forceinline__ void extract(uint32_t (&cnt)[32], uint32_t wt, uint32_t ngroups) {
     int nh = 0;
     while (nh < kOvNH && (ngroups >> nh) != 0) ++nh;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      uint32_t c = ((ones >> j) & 1u) | (((twos >> j) & 1u) << 1) | (((fours >> j) & 1u) << 2) |
-                   (((eights >> j) & 1u) << 3);
+      uint32_t c = ((ones >> j) & 1u) | (((twos >> j) & 1u) << 1) |
+                   (((fours >> j) & 1u) << 2) | (((eights >> j) & 1u) << 3);
 #pragma unroll
       for (int i = 0; i < kOvNH; ++i)
         if (i < nh) c += ((H[i] >> j) & 1u) << (4 + i);
       cnt[j] += wt * c;
     }
   }
-}
+};
 
 __global__ void __launch_bounds__(kOvThreads)
-    k_overlap(const OverlapArgs a) {
-  __shared__ uint32_t sh_hist[kHistSmemBins];
-  __shared__ uint32_t tb[kOvThreads / 32][32][33];
+    k_overlap(const __grid_constant__ CUtensorMap tm, const OverlapArgs a, int gather) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint32_t *stage = reinterpret_cast<uint32_t *>(sm);
+  uint32_t *sh_hist = stage + kOvStages * kOvStageWords;
+  uint32_t(*tb)[32][33] = reinterpret_cast<uint32_t(*)[32][33]>(sh_hist + kHistSmemBins);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sh_hist + kHistSmemBins + kOvTiles * 32 * 33);
   const int tid = threadIdx.x;
   const int wi = tid >> 5, lane = tid & 31;
   const bool do_hist = a.bins != nullptr;
   const bool sh_hist_on = do_hist && a.nbins <= kHistSmemBins;
   if (sh_hist_on)
     for (uint32_t i = tid; i < a.nbins; i += kOvThreads) sh_hist[i] = 0;
+  if (tid == 0) {
+    ptx::prefetch_tmap(&tm);
+    for (int s = 0; s < kOvStages; ++s) ptx::mbar_init(&full[s], 1);
+    ptx::fence_mbar_init();
+  }
   __syncthreads();
-  const uint64_t nwords = (a.pixels + 31) / 32;
-  const uint64_t ntiles = (nwords + kOvThreads - 1) / kOvThreads;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t w = tile * kOvThreads + tid;
-    const bool valid = w < nwords;
-    uint32_t cnt[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) cnt[j] = 0;
-    if (a.k1 && a.w1) count_range(a.packed, a.wpm, a.slots, 0, a.k1, w, valid, a.w1, cnt);
-    if (a.k2 && a.w2) count_range(a.packed, a.wpm, a.slots, a.k1, a.k2, w, valid, a.w2, cnt);
-    // transpose through SMEM so that stores are lane-contiguous
-#pragma unroll
-    for (int j = 0; j < 32; ++j) tb[wi][lane][j] = cnt[j];
-    __syncwarp();
-    const uint64_t wbase = tile * kOvThreads + (uint64_t)wi * 32;
-    for (int i = 0; i < 32; ++i) {
-      const uint64_t px = (wbase + i) * 32 + lane;
-      const bool pv = px < a.pixels;
-      const uint32_t c = tb[wi][i][lane];
-      if (pv) {
-        if (a.counts) a.counts[px] = c;
-        if (a.rgba) a.rgba[px] = rgba_word(c, a.n_inputs, a.lut);
-      }
-      if (do_hist) hist_add(c, pv && c < a.nbins, sh_hist_on ? sh_hist : nullptr, a.bins);
+
+  const uint64_t ntiles = a.wpm / 32;
+  const uint64_t ntg = (ntiles + kOvTiles - 1) / kOvTiles;
+  const uint32_t G1 = a.w1 ? (a.k1 + kOvGroup - 1) / kOvGroup : 0;
+  const uint32_t G2 = a.w2 ? (a.k2 + kOvGroup - 1) / kOvGroup : 0;
+  const uint32_t GP = G1 + G2;
+  const uint64_t nq = ntg > blockIdx.x ? (ntg - blockIdx.x - 1) / gridDim.x + 1 : 0;
+  const uint64_t nitems = nq * GP;
+
+  // item -> (tile group, slot offset, mask count)
+  auto decode = [&](uint64_t i, uint64_t &tg, uint32_t &off, uint32_t &cnt, uint32_t &g) {
+    const uint64_t q = i / GP;
+    g = (uint32_t)(i % GP);
+    tg = blockIdx.x + q * gridDim.x;
+    if (g < G1) {
+      off = g * kOvGroup;
+      cnt = min((uint32_t)kOvGroup, a.k1 - off);
+    } else {
+      const uint32_t gi = g - G1;
+      off = a.k1 + gi * kOvGroup;
+      cnt = min((uint32_t)kOvGroup, a.k2 - gi * kOvGroup);
     }
-    __syncwarp();
+  };
+  auto issue = [&](uint64_t i) {
+    uint64_t tg;
+    uint32_t off, cnt, g;
+    decode(i, tg, off, cnt, g);
+    const int s = (int)(i % kOvStages);
+    uint32_t *dst = stage + s * kOvStageWords;
+    if (!gather) {
+      ptx::mbar_arrive_expect_tx(&full[s], kOvStageWords * 4);
+      ptx::tma_load_3d(dst, &tm, 0, (int)off, (int)(tg * kOvTiles), &full[s]);
+    } else {
+      ptx::mbar_arrive_expect_tx(&full[s], cnt * kOvTiles * 32 * 4);
+      for (uint32_t j = 0; j < cnt; ++j)
+        ptx::tma_load_3d(dst + j * kOvTiles * 32, &tm, 0, (int)__ldg(a.slots + off + j),
+                         (int)(tg * kOvTiles), &full[s]);
+    }
+  };
+  if (tid == 0)
+    for (uint64_t i = 0; i < nitems && i < (uint64_t)kOvStages; ++i) issue(i);
+
+  HSCounter hc;
+  hc.reset();
+  uint32_t cnt32[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) cnt32[j] = 0;
+  uint32_t groups_in_pass = 0;
+
+  for (uint64_t i = 0; i < nitems; ++i) {
+    const int s = (int)(i % kOvStages);
+    uint64_t tg;
+    uint32_t off, cnt, g;
+    decode(i, tg, off, cnt, g);
+    ptx::mbar_wait(&full[s], (uint32_t)((i / kOvStages) & 1));
+    const uint32_t *st = stage + s * kOvStageWords;
+    uint32_t d[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int idx = gather ? ((j * kOvTiles + wi) * 32 + lane) : ((wi * kOvGroup + j) * 32 + lane);
+      d[j] = (j < (int)cnt) ? st[idx] : 0u;
+    }
+    __syncthreads();  // every thread has read stage s
+    if (tid == 0 && i + kOvStages < nitems) issue(i + kOvStages);
+    hc.add16(d);
+    ++groups_in_pass;
+    const bool range_end = (g == G1 - 1 && G1 > 0) || g == GP - 1;
+    if (range_end || groups_in_pass == kOvGroupsPerPass) {
+      hc.extract(cnt32, g < G1 ? a.w1 : a.w2, groups_in_pass);
+      hc.reset();
+      groups_in_pass = 0;
+    }
+    if (g == GP - 1) {
+      // epilogue for tile tg*4 + wi: transpose, then lane-contiguous stores
+#pragma unroll
+      for (int j = 0; j < 32; ++j) tb[wi][lane][j] = cnt32[j];
+      __syncwarp();
+      const uint64_t wbase = (tg * kOvTiles + wi) * 32;
+      for (int r = 0; r < 32; ++r) {
+        const uint64_t px = (wbase + r) * 32 + lane;
+        const bool pv = px < a.pixels;
+        const uint32_t c = tb[wi][r][lane];
+        if (pv) {
+          if (a.counts) a.counts[px] = c;
+          if (a.rgba) a.rgba[px] = rgba_word(c, a.n_inputs, a.lut);
+        }
+        if (do_hist) hist_add(c, pv && c < a.nbins, sh_hist_on ? sh_hist : nullptr, a.bins);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) cnt32[j] = 0;
+    }
   }
   __syncthreads();
   if (sh_hist_on)
@@ -459,42 +540,62 @@ __global__ void __launch_bounds__(kOvThreads)
 
 cudaError_t launch_overlap(const OverlapArgs &a, cudaStream_t s) {
   if (a.pixels == 0) return cudaSuccess;
-  const uint64_t nwords = (a.pixels + 31) / 32;
-  const uint64_t ntiles = (nwords + kOvThreads - 1) / kOvThreads;
+  const uint32_t k = a.k1 + a.k2;
+  const int64_t first = contiguous_run(a.host_slots, k);
+  CUtensorMap tm;
+  cudaError_t e;
+  const int gather = first < 0 ? 1 : 0;
+  const uint64_t ntiles = a.wpm / 32;
+  if (!gather)
+    e = encode_packed_map(&tm, a.packed, a.capacity, (uint64_t)first, k, ntiles, 32, kOvGroup,
+                          kOvTiles, 0);
+  else
+    e = encode_packed_map(&tm, a.packed, a.capacity, 0, a.capacity, ntiles, 32, 1, kOvTiles, 0);
+  if (e != cudaSuccess) return e;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_overlap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOvSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_overlap, kOvThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_overlap, kOvThreads, kOvSmem);
   if (per_sm < 1) per_sm = 1;
+  const uint64_t ntg = (ntiles + kOvTiles - 1) / kOvTiles;
   uint64_t grid = (uint64_t)num_sms() * per_sm;
-  if (grid > ntiles) grid = ntiles;
-  k_overlap<<<(unsigned)grid, kOvThreads, 0, s>>>(a);
+  if (grid > ntg) grid = ntg;
+  k_overlap<<<(unsigned)grid, kOvThreads, kOvSmem, s>>>(tm, a, gather);
   return cudaGetLastError();
 }
 
-// Per-item streaming accumulate (run_stream's kernel[i]): counts += bits of one mask.
-__global__ void k_accumulate_packed(const uint32_t *__restrict__ pk, uint64_t pixels,
-                                    uint32_t *__restrict__ counts) {
+// Per-item streaming accumulate (run_stream's kernel[i]): counts += bits of one
+// mask.  A warp takes one tile: one coalesced 128-B load, then word i is broadcast
+// and lane l adds bit l, so the counts stores are lane-contiguous.
+__global__ void k_accumulate_packed(const uint32_t *__restrict__ packed, uint64_t slot,
+                                    uint64_t cap, uint64_t pixels, uint32_t *__restrict__ counts) {
   const uint64_t nwords = (pixels + 31) / 32;
+  const uint64_t ntiles = (nwords + 31) / 32;
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t w0 = warp * 32; w0 < nwords; w0 += nwarps * 32) {
-    const uint32_t mine = (w0 + lane < nwords) ? ptx::ld_nc_u32(pk + w0 + lane) : 0u;
+  for (uint64_t t = warp; t < ntiles; t += nwarps) {
+    const uint32_t mine = ptx::ld_nc_u32(packed + (t * cap + slot) * 32 + lane);
     for (int i = 0; i < 32; ++i) {
       const uint32_t wd = __shfl_sync(0xffffffffu, mine, i);
-      const uint64_t px = (w0 + i) * 32 + lane;
+      const uint64_t px = (t * 32 + i) * 32 + lane;
       if (px < pixels) counts[px] += (wd >> lane) & 1u;
     }
   }
 }
 
-cudaError_t launch_accumulate_packed(const uint32_t *packed_mask, uint64_t pixels,
-                                     uint32_t *counts, cudaStream_t s) {
+cudaError_t launch_accumulate_packed(const uint32_t *packed, uint64_t slot, uint64_t cap,
+                                     uint64_t pixels, uint32_t *counts, cudaStream_t s) {
   if (pixels == 0) return cudaSuccess;
-  const uint64_t nwords = (pixels + 31) / 32;
-  uint64_t grid = (nwords + 255) / 256;
-  uint64_t cap = (uint64_t)num_sms() * 8;
-  if (grid > cap) grid = cap;
-  k_accumulate_packed<<<(unsigned)grid, 256, 0, s>>>(packed_mask, pixels, counts);
+  const uint64_t ntiles = ((pixels + 31) / 32 + 31) / 32;
+  uint64_t grid = (ntiles + 7) / 8;
+  uint64_t cap_grid = (uint64_t)num_sms() * 8;
+  if (grid > cap_grid) grid = cap_grid;
+  k_accumulate_packed<<<(unsigned)grid, 256, 0, s>>>(packed, slot, cap, pixels, counts);
   return cudaGetLastError();
 }
 
@@ -505,7 +606,7 @@ constexpr int kGpTile = 64;
 constexpr int kGpSlab = 32;
 
 __global__ void __launch_bounds__(256)
-    k_gram_popc(const uint32_t *__restrict__ packed, uint64_t wpm,
+    k_gram_popc(const uint32_t *__restrict__ packed, uint64_t cap, uint64_t wpm,
                 const uint32_t *__restrict__ slots, uint32_t k, uint32_t nb, uint64_t kchunk,
                 unsigned long long *__restrict__ gram) {
   __shared__ uint32_t A[kGpTile][kGpSlab + 1];
@@ -530,8 +631,8 @@ __global__ void __launch_bounds__(256)
       const int r = idx / kGpSlab, c = idx % kGpSlab;
       const uint32_t ra = I * kGpTile + r, rb = J * kGpTile + r;
       const bool kin = kb + c < k1;
-      A[r][c] = (ra < k && kin) ? __ldg(packed + (uint64_t)__ldg(slots + ra) * wpm + kb + c) : 0u;
-      B[r][c] = (rb < k && kin) ? __ldg(packed + (uint64_t)__ldg(slots + rb) * wpm + kb + c) : 0u;
+      A[r][c] = (ra < k && kin) ? __ldg(packed + pk_off(__ldg(slots + ra), kb + c, cap)) : 0u;
+      B[r][c] = (rb < k && kin) ? __ldg(packed + pk_off(__ldg(slots + rb), kb + c, cap)) : 0u;
     }
     __syncthreads();
 #pragma unroll 8
@@ -557,8 +658,9 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-cudaError_t launch_gram_popc(const uint32_t *packed, uint64_t wpm, const uint32_t *slots,
-                             uint32_t k, unsigned long long *gram, cudaStream_t s) {
+cudaError_t launch_gram_popc(const uint32_t *packed, uint64_t cap, uint64_t wpm,
+                             const uint32_t *slots, uint32_t k, unsigned long long *gram,
+                             cudaStream_t s) {
   if (k == 0) return cudaSuccess;
   const uint32_t nb = (k + kGpTile - 1) / kGpTile;
   const uint32_t ntiles = nb * (nb + 1) / 2;
@@ -573,7 +675,7 @@ cudaError_t launch_gram_popc(const uint32_t *packed, uint64_t wpm, const uint32_
     kchunk = ((wpm + ksplit - 1) / ksplit + kGpSlab - 1) / kGpSlab * kGpSlab;
   }
   dim3 grid(ntiles, (unsigned)ksplit);
-  k_gram_popc<<<grid, 256, 0, s>>>(packed, wpm, slots, k, nb, kchunk, gram);
+  k_gram_popc<<<grid, 256, 0, s>>>(packed, cap, wpm, slots, k, nb, kchunk, gram);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_gram_mirror(gram, k, kGpTile, s);
@@ -602,8 +704,9 @@ cudaError_t launch_gram_mirror(unsigned long long *gram, uint32_t k, uint32_t ti
 // ---------------------------------------------------------------------------
 // Synthetic masks generated straight into the packed layout
 // ---------------------------------------------------------------------------
-__global__ void k_synth_packed(uint32_t *__restrict__ dst, uint64_t wpm, SynthParams sp,
-                               uint64_t mask, uint64_t row0, uint64_t pixels) {
+__global__ void k_synth_packed(uint32_t *__restrict__ dst, uint64_t slot, uint64_t cap,
+                               uint64_t wpm, SynthParams sp, uint64_t mask, uint64_t row0,
+                               uint64_t pixels) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < wpm; w += stride) {
     uint32_t word = 0;
@@ -620,18 +723,54 @@ __global__ void k_synth_packed(uint32_t *__restrict__ dst, uint64_t wpm, SynthPa
         }
       }
     }
-    dst[w] = word;
+    dst[pk_off(slot, w, cap)] = word;
   }
 }
 
-cudaError_t launch_synth_packed(uint32_t *dst, uint64_t wpm, const SynthParams &sp,
-                                uint64_t mask, uint64_t row0, uint64_t pixels,
-                                cudaStream_t s) {
+cudaError_t launch_synth_packed(uint32_t *dst, uint64_t slot, uint64_t cap, uint64_t wpm,
+                                const SynthParams &sp, uint64_t mask, uint64_t row0,
+                                uint64_t pixels, cudaStream_t s) {
   uint64_t grid = (wpm + 255) / 256;
-  uint64_t cap = (uint64_t)num_sms() * 16;
-  if (grid > cap) grid = cap;
-  k_synth_packed<<<(unsigned)grid, 256, 0, s>>>(dst, wpm, sp, mask, row0, pixels);
+  const uint64_t gcap = (uint64_t)num_sms() * 16;
+  if (grid > gcap) grid = gcap;
+  k_synth_packed<<<(unsigned)grid, 256, 0, s>>>(dst, slot, cap, wpm, sp, mask, row0, pixels);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Host: TMA tensor maps over the packed layout
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+cudaError_t encode_packed_map(CUtensorMap *out, const uint32_t *packed, uint64_t capacity,
+                              uint64_t row0, uint64_t rows, uint64_t ntiles, uint32_t box_words,
+                              uint32_t box_rows, uint32_t box_tiles, int swizzle) {
+  if (g_encode == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || fn == nullptr) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[3] = {32, rows > 0 ? rows : 1, ntiles > 0 ? ntiles : 1};
+  cuuint64_t strides[2] = {128, capacity * 128};
+  cuuint32_t box[3] = {box_words, box_rows, box_tiles};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMapSwizzle sw = swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                          : CU_TENSOR_MAP_SWIZZLE_NONE;
+  void *base = const_cast<uint32_t *>(packed) + row0 * 32;
+  CUresult r = g_encode(out, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+int64_t contiguous_run(const uint32_t *host_slots, uint32_t k) {
+  if (k == 0 || host_slots == nullptr) return -1;
+  for (uint32_t i = 1; i < k; ++i)
+    if (host_slots[i] != host_slots[0] + i) return -1;
+  return host_slots[0];
 }
 
 // ---------------------------------------------------------------------------

@@ -122,6 +122,10 @@ class DeviceEnsemble:
         N.call("fs_ensemble_stream_handle", self._h, C.byref(p))
         return p.value or 0
 
+    def use_stream(self, stream_ptr: int | None) -> None:
+        """Run compute work on a caller-owned CUDA stream (None: the ensemble's own)."""
+        N.call("fs_ensemble_set_stream", self._h, stream_ptr or None)
+
     def sync(self) -> None:
         N.call("fs_ensemble_sync", self._h)
 
