@@ -1,0 +1,177 @@
+"""Multi-GPU sharding of the overlap path: one process per GPU, row bands of every mask.
+
+SURVEY §8(e): the per-pixel products (counts, histogram, composite) have no stencil
+and no halo, and the Gram is a sum over pixels, so the ensemble shards by spatial ROW
+BANDS — rank r owns rows [row0_r, row0_r + rows_r) of every mask (one contiguous H2D
+per mask, one contiguous slice of every output).  The only exchange is one bucketed
+``all_reduce(sum)`` of the int64 partials [histogram | Gram] (8 (n+1) + 8 k^2 bytes;
+8 MiB at 1024 masks); counts/RGBA bands stay on their rank or are gathered to rank 0
+(``gather_rows``).  Jaccard, outliers and clusters then run on the exact summed Gram,
+so every rank (or rank 0 alone) produces results bit-identical to one GPU.
+
+Reference: the partitioning ``north_star`` prescribes ("spatial tiles sharded across
+GPUs ... partial Gram matrices summed with NCCL allreduce"); the single-device
+semantics are fs/analytics.py:106-240 and fs/service.py:143-175.
+
+The collective helpers take torch tensors and a process group, so the same code runs
+over NCCL on B200s and over gloo on CPU in the tests.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def band(height: int, rank: int, world: int) -> tuple[int, int]:
+    """(row0, rows) of rank's band: rows split as evenly as possible, lower ranks first."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    base, extra = divmod(int(height), int(world))
+    row0 = rank * base + min(rank, extra)
+    return row0, base + (1 if rank < extra else 0)
+
+
+def partial_layout(k: int, n_inputs: int | None = None) -> tuple[int, int]:
+    """Offsets of the bucketed int64 partial buffer: bins at [0, n+1), Gram after."""
+    nb = (k if n_inputs is None else n_inputs) + 1
+    return nb, nb + k * k
+
+
+def allreduce_partials(buf, group=None) -> None:
+    """Sum the bucketed int64 [bins | Gram] partial buffer over all ranks, in place.
+    One collective per recompute (launch latency, not link count, dominates at 8 MiB)."""
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+
+
+def gather_rows(local, height: int, group=None, dst: int = 0):
+    """Assemble per-rank row bands (first dim = rows of the band) into the full raster on
+    ``dst`` (other ranks get None).  Bands are padded to the largest band for the
+    collective and trimmed on arrival."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return local
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    rmax = band(height, 0, world)[1]
+    pad = torch.zeros((rmax,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    dist.gather(pad, parts, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([parts[r][: band(height, r, world)[1]] for r in range(world)], dim=0)
+
+
+class ShardedEnsemble:
+    """This rank's row band of a bit-packed ensemble plus the exchange step.
+
+    ``recompute()`` runs the fused overlap pass and the Gram on this rank's band with
+    device outputs written straight into one bucketed buffer, sums the partials with a
+    single all-reduce on the ensemble's stream, and returns host (numpy) results:
+    this band's counts and RGBA, and the GLOBAL histogram and Gram.
+    """
+
+    def __init__(self, width: int, height: int, capacity: int, *, group=None,
+                 device: int | None = None):
+        import torch
+        import torch.distributed as dist
+
+        from .ensemble import DeviceEnsemble
+
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.width, self.height = int(width), int(height)
+        self.row0, self.rows = band(height, self.rank, self.world)
+        dev = torch.cuda.current_device() if device is None else int(device)
+        self.device = torch.device("cuda", dev)
+        self.ens = DeviceEnsemble(width, height, capacity, row0=self.row0, rows=self.rows,
+                                  device=dev)
+        self.stream = torch.cuda.Stream(device=self.device)
+        self.ens.use_stream(self.stream.cuda_stream)
+        self.capacity = int(capacity)
+        self._bufs = {}
+
+    def close(self) -> None:
+        self.ens.close()
+
+    def _buffers(self, k: int, n_inputs: int):
+        import torch
+
+        key = (k, n_inputs)
+        if key not in self._bufs:
+            nb, total = partial_layout(k, n_inputs)
+            px = self.rows * self.width
+            self._bufs = {key: dict(
+                part=torch.empty(total, dtype=torch.int64, device=self.device),
+                counts=torch.empty(px, dtype=torch.int32, device=self.device),
+                rgba=torch.empty(px * 4, dtype=torch.uint8, device=self.device),
+                h_part=torch.empty(total, dtype=torch.int64).pin_memory(),
+                nb=nb)}
+        return self._bufs[key]
+
+    def recompute_device(self, slots, *, engine: str = "auto", cycles: int = 1,
+                         remainder: int = 0, counts: bool = True, rgba: bool = True):
+        """Enqueue one recompute on the ensemble stream; returns the device buffers.
+        Nothing is synchronised: the all-reduce is ordered after the kernels on the
+        same stream."""
+        import torch
+
+        sl = np.asarray(list(slots), dtype=np.uint32)
+        k = int(sl.size)
+        n_inputs = cycles * k + remainder
+        b = self._buffers(k, n_inputs)
+        nb = b["nb"]
+        part = b["part"]
+        self.ens.overlap(sl, cycles=cycles, remainder=remainder,
+                         out_counts=b["counts"].data_ptr() if counts else None,
+                         out_rgba=b["rgba"].data_ptr() if rgba else None,
+                         out_bins=part.data_ptr(), counts=counts, rgba=rgba,
+                         device_outputs=True)
+        self.ens.gram(sl, engine=engine, out=part.data_ptr() + nb * 8, device_outputs=True)
+        with torch.cuda.stream(self.stream):
+            allreduce_partials(part, self.group)
+        return b
+
+    def fetch(self, b, *, counts: bool = True, rgba: bool = True):
+        """D2H of the summed partials (and this band's maps) on the ensemble stream."""
+        import torch
+
+        k2 = b["part"].numel() - b["nb"]
+        k = int(round(k2 ** 0.5))
+        with torch.cuda.stream(self.stream):
+            b["h_part"].copy_(b["part"], non_blocking=True)
+            hc = hr = None
+            if counts:
+                hc = torch.empty(b["counts"].shape, dtype=torch.int32, pin_memory=True)
+                hc.copy_(b["counts"], non_blocking=True)
+            if rgba:
+                hr = torch.empty(b["rgba"].shape, dtype=torch.uint8, pin_memory=True)
+                hr.copy_(b["rgba"], non_blocking=True)
+        self.stream.synchronize()
+        part = b["h_part"].numpy()
+        bins = part[: b["nb"]].copy()
+        gram = part[b["nb"]:].reshape(k, k).copy()
+        c = hc.numpy().view(np.uint32).reshape(self.rows, self.width) if counts else None
+        r = hr.numpy().reshape(self.rows, self.width, 4) if rgba else None
+        return c, bins, r, gram
+
+    def recompute(self, slots, *, tau: float = 0.8, engine: str = "auto", ids=None):
+        """Full recompute: band maps + global histogram, Gram, similarity, outliers and
+        clusters (identical on every rank)."""
+        from .analytics import cluster_from_similarity, outliers_from_similarity, similarity_from_gram
+
+        b = self.recompute_device(slots, engine=engine)
+        c, bins, r, gram = self.fetch(b)
+        sl = list(slots)
+        ids = ids or [f"s{i:04d}" for i in sl]
+        sim = similarity_from_gram(gram)
+        outl = outliers_from_similarity(sim, ids) if len(ids) >= 2 else None
+        clus = cluster_from_similarity(sim, ids, tau)
+        return {"counts": c, "bins": bins, "rgba": r, "gram": gram, "similarity": sim,
+                "outliers": outl, "clusters": clus}
