@@ -284,6 +284,36 @@ def band(height, rank, world):
     return row0, base + (1 if rank < extra else 0)
 
 
+def pcie_h2d_gbs(nbytes: int = 1 << 30, reps: int = 5) -> float:
+    """Measured pinned host->device copy bandwidth (GB/s, best of reps, CUDA events):
+    the e2e roofline denominator (fs/bench.py:193-228's transfer baseline, measured)."""
+    import torch
+
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    del h, d
+    return nbytes / best / 1e9
+
+
+def load_traffic() -> dict:
+    """dram bytes per launch from the committed ncu --set full captures (profiles/)."""
+    p = REPO / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            pass
+    return {}
+
+
 def main():
     args = parse()
     width, height, k, members, eps = CONFIGS[args.config]
@@ -298,10 +328,7 @@ def main():
     import torch
 
     from paper_2104_14667_b200 import _native as N
-    from paper_2104_14667_b200.analytics import (cluster_from_similarity,
-                                                 outliers_from_similarity,
-                                                 similarity_from_gram)
-    from paper_2104_14667_b200.ensemble import DeviceEnsemble
+    from paper_2104_14667_b200.dist import ShardedEnsemble
     from paper_2104_14667_b200.synth import synth_cells
 
     torch.cuda.set_device(local_rank)
@@ -311,43 +338,17 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    row0, rows = band(height, rank, world)
-    P_band = rows * width
+    dev = torch.device("cuda", local_rank)
     P = width * height
     slots = list(range(k))
     ids = [f"s{i:04d}" for i in range(k)]
 
-    ens = DeviceEnsemble(width, height, k, row0=row0, rows=rows)
+    sh = ShardedEnsemble(width, height, k)
+    row0, rows = sh.row0, sh.rows
+    P_band = rows * width
+    ens = sh.ens
     ens.synth(0, k, seed=2104, members=members, eps=eps)
-    # the ensemble's compute work runs on a torch-owned stream, so collectives, copies
-    # and timing events are ordered with it and its lifetime is torch's
-    stream = torch.cuda.Stream()
-    ens.use_stream(stream.cuda_stream)
-    dev = torch.device("cuda", local_rank)
-    d_counts = torch.empty(P_band, dtype=torch.int32, device=dev)
-    d_rgba = torch.empty(P_band * 4, dtype=torch.uint8, device=dev)
-    d_bins = torch.empty(k + 1, dtype=torch.int64, device=dev)
-    d_gram = torch.empty((k, k), dtype=torch.int64, device=dev)
-    h_bins = torch.empty(k + 1, dtype=torch.int64).pin_memory()
-    h_gram = torch.empty((k, k), dtype=torch.int64).pin_memory()
-
-    def device_step():
-        ens.overlap(slots, out_counts=d_counts.data_ptr(), out_rgba=d_rgba.data_ptr(),
-                    out_bins=d_bins.data_ptr(), device_outputs=True)
-        ens.gram(slots, engine=args.engine, out=d_gram.data_ptr(), device_outputs=True)
-        with torch.cuda.stream(stream):
-            if dist is not None:
-                dist.all_reduce(d_bins)
-                dist.all_reduce(d_gram)
-            h_bins.copy_(d_bins, non_blocking=True)
-            h_gram.copy_(d_gram, non_blocking=True)
-
-    def host_step():
-        stream.synchronize()
-        if rank == 0:
-            sim = similarity_from_gram(h_gram.numpy())
-            outliers_from_similarity(sim, ids)
-            cluster_from_similarity(sim, ids, args.tau)
+    stream = sh.stream
 
     def barrier():
         torch.cuda.synchronize()
@@ -362,102 +363,121 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- resident timed region ----------------------------------------------------
-    for _ in range(args.warmup):
-        device_step()
-        host_step()
+    kern = {"overlap": [], "gram": []}
+
+    def sample_kernels(_f):
+        # per-kernel CUDA-event durations of the previous frame (ensemble stream)
+        if _f > 0:
+            kern["overlap"].append(ens.kernel_ms("overlap"))
+            kern["gram"].append(ens.kernel_ms("gram"))
+
+    # ---- resident timed region: K pipelined full recomputes ---------------------------
+    sh.run_frames(slots, args.warmup, tau=args.tau, engine=args.engine, ids=ids,
+                  analytics_ranks="root", keep=False)
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    kern = {"overlap": [], "gram": []}
+    host_ms = []
     with Clocks(local_rank) as clk:
         barrier()
         ev0.record(stream)
-        for _ in range(args.steps):
-            device_step()
-            host_step()
-            kern["overlap"].append(ens.kernel_ms("overlap"))
-            kern["gram"].append(ens.kernel_ms("gram"))
+        t_wall0 = time.perf_counter()
+        last = sh.run_frames(slots, args.steps, tau=args.tau, engine=args.engine, ids=ids,
+                             analytics_ranks="root", keep=False)
         ev1.record(stream)
         ev1.synchronize()
+        t_wall = time.perf_counter() - t_wall0
         barrier()
     t_res = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
     clocks = clk.summary()
     ms_step = t_res / args.steps * 1e3
     value = k * P * args.steps / t_res / 1e9
+    if rank == 0:  # host analytics cost of one frame, timed apart (it overlaps the GPU)
+        from paper_2104_14667_b200.analytics import (cluster_from_similarity,
+                                                     outliers_from_similarity,
+                                                     similarity_from_gram)
 
-    # ---- per-kernel roofline ---------------------------------------------------------
+        for _ in range(3):
+            t0 = time.perf_counter()
+            sim = similarity_from_gram(last[0]["gram"])
+            outliers_from_similarity(sim, ids)
+            n_clusters = len(cluster_from_similarity(sim, ids, args.tau))
+            host_ms.append((time.perf_counter() - t0) * 1e3)
+
+    # ---- per-kernel roofline: CUDA-event durations on the ensemble stream, sampled in
+    # extra untimed frames (reading them blocks, which would break the pipelining) ----
+    sh.run_frames(slots, 6, tau=args.tau, engine=args.engine, ids=ids, analytics_ranks="none",
+                  keep=False, before_frame=sample_kernels)
+    sample_kernels(1)
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    bf16 = float(peaks.get("bf16_tflops", 1590.0))
-    i8_peak = 2.0 * bf16  # dense int8 MMA issues at twice the bf16 rate on sm_100
+    traffic = load_traffic()
     ov_ms = statistics.median(kern["overlap"])
     gr_ms = statistics.median(kern["gram"])
     ov_bytes = k * P_band / 8 + 4 * P_band + 4 * P_band + 8 * (k + 1)
-    gram_ops = 2.0 * k * k * P_band
+    gram_ops = float(k) * (k + 1) * P_band  # upper triangle incl. diagonal, MAC = 2 ops
+    i8_peak = 4500.0  # dense int8 tcgen05, TOPS (B200_PROFILING.md fallback table)
     rl_over = {"bound": "hbm", "achieved": round(ov_bytes / ov_ms / 1e6, 1), "peak": hbm,
-               "unit": "GB/s", "frac": round(ov_bytes / ov_ms / 1e6 / hbm, 4), "traffic": None,
-               "kernel_ms": round(ov_ms, 4), "bytes_per_launch": int(ov_bytes)}
+               "unit": "GB/s", "frac": round(ov_bytes / ov_ms / 1e6 / hbm, 4),
+               "traffic": traffic.get("k_overlap"), "kernel_ms": round(ov_ms, 4),
+               "bytes_per_launch": int(ov_bytes),
+               "bytes_def": "N*P/8 packed read + 4P counts + 4P RGBA + 8(N+1) bins",
+               "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy test)"}
     rl_gram = {"bound": "tensor", "achieved": round(gram_ops / gr_ms / 1e9, 1), "peak": i8_peak,
                "unit": "TFLOP/s", "frac": round(gram_ops / gr_ms / 1e9 / i8_peak, 4),
-               "traffic": None, "kernel_ms": round(gr_ms, 4), "ops_per_launch": gram_ops,
-               "ops_def": "2*N^2*P (full Gram, int8 MAC = 2 ops)",
-               "peak_note": "int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json)"}
+               "traffic": traffic.get("k_gram_tc"), "kernel_ms": round(gr_ms, 4),
+               "ops_per_launch": gram_ops,
+               "ops_def": "N(N+1)*P = 2 ops x the N(N+1)/2 distinct mask pairs x P px",
+               "peak_note": "dense int8 4.5 POPS (no measured int8 peak in MEASURED_PEAKS.json)"}
     dominant = rl_gram if gr_ms >= ov_ms else rl_over
 
     # ---- end-to-end through the public API from pinned host rasters --------------------
     e2e = None
+    host = h_counts = None
     if not args.no_e2e:
         host = [N.PinnedBuffer((P_band,)) for _ in range(k)]
         for i in range(k):
             synth_cells(width, height, i, seed=2104, members=members, eps=eps, row0=row0,
                         rows=rows, out=host[i].array.reshape(rows, width))
-        h_counts = N.PinnedBuffer((rows, width), np.uint32)
-        h_rgba = N.PinnedBuffer((rows, width, 4), np.uint8)
         arrays = [h.array for h in host]
 
-        def e2e_step():
+        def upload(_f):
             ens.stream(arrays, variant="2b-final", already_banded=True)
-            ens.overlap(slots, out_counts=d_counts.data_ptr(), out_rgba=d_rgba.data_ptr(),
-                        out_bins=d_bins.data_ptr(), device_outputs=True)
-            ens.gram(slots, engine=args.engine, out=d_gram.data_ptr(), device_outputs=True)
-            with torch.cuda.stream(stream):
-                if dist is not None:
-                    dist.all_reduce(d_bins)
-                    dist.all_reduce(d_gram)
-                torch.from_numpy(h_counts.array.reshape(-1).view(np.int32)).copy_(
-                    d_counts, non_blocking=True)
-                torch.from_numpy(h_rgba.array.reshape(-1)).copy_(d_rgba, non_blocking=True)
-                h_bins.copy_(d_bins, non_blocking=True)
-                h_gram.copy_(d_gram, non_blocking=True)
-            host_step()
 
-        e2e_step()  # warm-up
+        sh.run_frames(slots, 1, tau=args.tau, engine=args.engine, ids=ids, maps_to_host=True,
+                      analytics_ranks="root", keep=False, before_frame=upload)  # warm-up
         barrier()
         ev0.record(stream)
-        for _ in range(args.e2e_steps):
-            e2e_step()
+        res = sh.run_frames(slots, args.e2e_steps, tau=args.tau, engine=args.engine, ids=ids,
+                            maps_to_host=True, analytics_ranks="root", keep=False,
+                            before_frame=upload)
         ev1.record(stream)
         ev1.synchronize()
         barrier()
         t_e2e = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
-        # parity spot check of the streamed path against the host oracle bytes
+        h2d = int(k * P_band)
+        pcie = pcie_h2d_gbs()
+        t_min = h2d / (pcie * 1e9)
         e2e = {"value": round(k * P * args.e2e_steps / t_e2e / 1e9, 4), "unit": UNIT,
                "h2d_bytes_per_step": int(k * P),
-               "d2h_bytes_per_step": int(8 * P + world * (8 * (k + 1) + 8 * k * k)),
+               "d2h_bytes_per_step": int(8 * P + world * 8 * ((k + 1) + k * k)),
                "ms_per_step": round(t_e2e / args.e2e_steps * 1e3, 3),
                "fps": round(args.e2e_steps / t_e2e, 4), "steps": args.e2e_steps,
-               "path": "DeviceEnsemble.stream(2b-final, pinned) -> overlap -> gram -> D2H"}
+               "roofline": {"bound": "pcie_h2d", "achieved": round(h2d / (t_e2e / args.e2e_steps) / 1e9, 2),
+                            "peak": round(pcie, 2), "unit": "GB/s",
+                            "frac": round(t_min / (t_e2e / args.e2e_steps), 4),
+                            "peak_note": "measured pinned H2D, 1 GiB copy, best of 5"},
+               "path": "DeviceEnsemble.stream(2b-final, pinned) -> overlap -> gram -> D2H "
+                       "counts+RGBA+bins+Gram -> Jaccard/outliers/clusters"}
+        h_counts = res[-1].get("counts")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        src = host if e2e is not None else None
-        if src is None:
-            src = [type("B", (), {"array": synth_cells(width, height, i, seed=2104,
-                                                        members=members, eps=eps, rows=256)})()
-                   for i in range(k)]
-        window = min(P, 1 << 22)
-        cpu = cpu_baseline([b.array for b in src], width, height, k, min(window, src[0].array.size))
+        src = [b.array for b in host] if host is not None else [
+            synth_cells(width, height, i, seed=2104, members=members, eps=eps, rows=256)
+            for i in range(k)]
+        window = min(P, 1 << 22, src[0].size)
+        cpu = cpu_baseline(src, width, height, k, window)
 
     if rank == 0:
         line = {
@@ -470,8 +490,13 @@ def main():
                        "masks": k, "width": width, "height": height, "tau": args.tau,
                        "gram_engine": args.engine,
                        "parallelism": f"row-bands x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs (bit-packed 2.15 GB) larger than L2; no flush"},
+                       "l2": "inputs (bit-packed 2.15 GB) larger than L2; no flush",
+                       "pipelining": "double-buffered frames: host analytics of frame f "
+                                     "overlap device work of frame f+1"},
             "fps": round(args.steps / t_res, 3),
+            "wall_ms_per_step": round(t_wall / args.steps * 1e3, 4),
+            "host_analytics_ms": round(statistics.median(host_ms), 4) if host_ms else None,
+            "clusters": n_clusters if host_ms else None,
             "roofline": dominant,
             "kernels": {"overlap": rl_over, "gram": rl_gram},
             "clocks": clocks,
@@ -488,9 +513,9 @@ def main():
         line["gpu_launches"] = (1 + gram_launches) * args.steps
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
-    ens.close()
-    if e2e is not None:
-        for b in host + [h_counts, h_rgba]:
+    sh.close()
+    if host is not None:
+        for b in host:
             b.free()
     if dist is not None:
         dist.destroy_process_group()

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <limits>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -929,29 +930,35 @@ int fs_gram_many(const uint8_t *const *cells, uint32_t k, uint64_t n, int64_t *g
 // ---------------------------------------------------------------------------
 int fs_similarity_from_gram(const int64_t *gram, uint32_t n, double *sim) {
   if (!gram || !sim) return set_err(FS_EINVAL, "null buffer");
+  // analytics.py:165-171: union == 0 -> 1.0, else exact int/int true division (both
+  // operands are exact in double below 2^53, so IEEE division rounds like Python's).
   for (uint32_t i = 0; i < n; ++i) {
-    sim[(size_t)i * n + i] = 1.0;
+    const int64_t gii = gram[(size_t)i * n + i];
+    const int64_t *gr = gram + (size_t)i * n;
+    double *sr = sim + (size_t)i * n;
+    sr[i] = 1.0;
     for (uint32_t j = i + 1; j < n; ++j) {
-      const int64_t inter = gram[(size_t)i * n + j];
-      const int64_t uni = gram[(size_t)i * n + i] + gram[(size_t)j * n + j] - inter;
-      // analytics.py:165-171: union == 0 -> 1.0, else exact int/int true division
-      const double v = uni == 0 ? 1.0 : (double)inter / (double)uni;
-      sim[(size_t)i * n + j] = v;
-      sim[(size_t)j * n + i] = v;
+      const int64_t inter = gr[j];
+      const int64_t uni = gii + gram[(size_t)j * n + j] - inter;
+      sr[j] = uni == 0 ? 1.0 : (double)inter / (double)uni;
     }
   }
+  for (uint32_t i = 0; i < n; ++i)  // mirror (row-major writes, column reads)
+    for (uint32_t j = 0; j < i; ++j) sim[(size_t)i * n + j] = sim[(size_t)j * n + i];
   return FS_OK;
 }
 
 int fs_outlier_scores(const double *sim, uint32_t n, double *scores) {
   if (!sim || !scores) return set_err(FS_EINVAL, "null buffer");
   if (n < 2) return set_err(FS_EINVAL, "outlier scores need at least two surfaces");
+  // analytics.py:237-239: builtin sum() over np.float64 = plain left-to-right adds in
+  // ascending j (this TU is built without fast-math, so no reassociation/contraction).
   for (uint32_t i = 0; i < n; ++i) {
-    volatile double s = 0.0;  // left to right, ascending j (analytics.py:237-239)
-    for (uint32_t j = 0; j < n; ++j)
-      if (j != i) s = s + sim[(size_t)i * n + j];
-    volatile double mean = s / (double)(n - 1);
-    scores[i] = 1.0 - mean;
+    const double *r = sim + (size_t)i * n;
+    double s = 0.0;
+    for (uint32_t j = 0; j < i; ++j) s += r[j];
+    for (uint32_t j = i + 1; j < n; ++j) s += r[j];
+    scores[i] = 1.0 - s / (double)(n - 1);
   }
   return FS_OK;
 }
@@ -960,95 +967,97 @@ int fs_outlier_scores(const double *sim, uint32_t n, double *scores) {
 // (-score, lo_rank, hi_rank, a, b) over list positions a < b with score >= tau
 // (analytics.py:205-222).  List positions keep their relative order under deletion,
 // so a cluster's "slot" (original index of its list entry) stands in for a position.
-// Each slot caches its best partner; a merge only invalidates keys that involve the
-// merged slot, so most slots update in O(1).
-namespace {
-struct Key {
-  double score;
-  uint32_t lo, hi, a, b;
-  bool valid;
-};
-inline bool key_less(const Key &x, const Key &y) {
-  if (!x.valid) return false;
-  if (!y.valid) return true;
-  if (x.score != y.score) return x.score > y.score;
-  if (x.lo != y.lo) return x.lo < y.lo;
-  if (x.hi != y.hi) return x.hi < y.hi;
-  if (x.a != y.a) return x.a < y.a;
-  return x.b < y.b;
-}
-}  // namespace
-
+// Each live slot caches its best partner (scan of one linkage row); a merge (a, b),
+// b into a, lowers row a to min(L[a], L[b]) (Lance-Williams for complete linkage), so
+// only slots whose cached partner was a or b need a rescan; every other slot compares
+// its cache against the new (x, a) key.  Scores are compared first; the lexical
+// tie-break is evaluated only on exact score ties.
 int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *id_rank,
                                 double tau, int32_t *label) {
   if (!sim || !id_rank || !label) return set_err(FS_EINVAL, "null buffer");
   if (!(tau > 0.0 && tau <= 1.0)) return set_err(FS_EINVAL, "tau must be in (0, 1]");
+  constexpr uint32_t NONE = UINT32_MAX;
   std::vector<double> L(sim, sim + (size_t)n * n);
   std::vector<uint32_t> minr(id_rank, id_rank + n);
   std::vector<int32_t> owner(n);  // surface -> slot
   for (uint32_t i = 0; i < n; ++i) owner[i] = (int32_t)i;
-  std::vector<char> alive(n, 1);
-  std::vector<Key> best(n);
-  std::vector<uint32_t> best_of(n, UINT32_MAX);
-  auto key = [&](uint32_t x, uint32_t y) {
-    Key k;
-    k.score = L[(size_t)x * n + y];
-    k.valid = k.score >= tau;
-    k.lo = std::min(minr[x], minr[y]);
-    k.hi = std::max(minr[x], minr[y]);
-    k.a = std::min(x, y);
-    k.b = std::max(x, y);
-    return k;
+  std::vector<uint32_t> live(n);  // ascending live slots
+  for (uint32_t i = 0; i < n; ++i) live[i] = i;
+  std::vector<double> bs(n, 0.0);
+  std::vector<uint32_t> by(n, NONE);
+  // (x1, y1) before (x2, y2) at equal score
+  auto tie_less = [&](uint32_t x1, uint32_t y1, uint32_t x2, uint32_t y2) {
+    const uint32_t lo1 = std::min(minr[x1], minr[y1]), hi1 = std::max(minr[x1], minr[y1]);
+    const uint32_t lo2 = std::min(minr[x2], minr[y2]), hi2 = std::max(minr[x2], minr[y2]);
+    if (lo1 != lo2) return lo1 < lo2;
+    if (hi1 != hi2) return hi1 < hi2;
+    const uint32_t a1 = std::min(x1, y1), a2 = std::min(x2, y2);
+    if (a1 != a2) return a1 < a2;
+    return std::max(x1, y1) < std::max(x2, y2);
   };
-  auto recompute = [&](uint32_t x) {
-    Key b;
-    b.valid = false;
-    uint32_t arg = UINT32_MAX;
-    for (uint32_t y = 0; y < n; ++y) {
-      if (y == x || !alive[y]) continue;
-      Key k = key(x, y);
-      if (key_less(k, b)) {
-        b = k;
-        arg = y;
-      }
+  auto better = [&](double s1, uint32_t x1, uint32_t y1, double s2, uint32_t x2, uint32_t y2) {
+    if (y2 == NONE) return y1 != NONE;
+    if (y1 == NONE) return false;
+    if (s1 != s2) return s1 > s2;
+    return tie_less(x1, y1, x2, y2);
+  };
+  // Dead slots and the diagonal read as -inf, so a rescan is a branch-free max over
+  // one contiguous row (4 independent chains), then a pass over the exact ties.
+  const double NEG = -std::numeric_limits<double>::infinity();
+  for (uint32_t x = 0; x < n; ++x) L[(size_t)x * n + x] = NEG;
+  auto rescan = [&](uint32_t x) {
+    const double *row = L.data() + (size_t)x * n;
+    double m0 = NEG, m1 = NEG, m2 = NEG, m3 = NEG;
+    uint32_t y = 0;
+    for (; y + 4 <= n; y += 4) {
+      m0 = row[y] > m0 ? row[y] : m0;
+      m1 = row[y + 1] > m1 ? row[y + 1] : m1;
+      m2 = row[y + 2] > m2 ? row[y + 2] : m2;
+      m3 = row[y + 3] > m3 ? row[y + 3] : m3;
     }
-    best[x] = b;
-    best_of[x] = arg;
+    for (; y < n; ++y) m0 = row[y] > m0 ? row[y] : m0;
+    const double m = std::max(std::max(m0, m1), std::max(m2, m3));
+    uint32_t arg = NONE;
+    if (m >= tau) {
+      for (uint32_t z = 0; z < n; ++z)
+        if (row[z] == m && (arg == NONE || tie_less(x, z, x, arg))) arg = z;
+    }
+    bs[x] = m;
+    by[x] = arg;
   };
-  for (uint32_t x = 0; x < n; ++x) recompute(x);
-  uint32_t live = n;
-  while (live > 1) {
-    Key g;
-    g.valid = false;
-    uint32_t gx = UINT32_MAX;
-    for (uint32_t x = 0; x < n; ++x)
-      if (alive[x] && key_less(best[x], g)) {
-        g = best[x];
-        gx = x;
-      }
-    if (gx == UINT32_MAX) break;
-    const uint32_t a = g.a, b = g.b;  // a < b: b merges into a's list position
-    for (uint32_t y = 0; y < n; ++y) {
-      if (!alive[y] || y == a || y == b) continue;
-      const double v = std::min(L[(size_t)a * n + y], L[(size_t)b * n + y]);
-      L[(size_t)a * n + y] = v;
+  for (uint32_t x = 0; x < n; ++x) rescan(x);
+  while (live.size() > 1) {
+    uint32_t gx = NONE;
+    for (uint32_t x : live)
+      if (by[x] != NONE && (gx == NONE || better(bs[x], x, by[x], bs[gx], gx, by[gx]))) gx = x;
+    if (gx == NONE) break;
+    const uint32_t a = std::min(gx, by[gx]), b = std::max(gx, by[gx]);  // b merges into a
+    double *ra = L.data() + (size_t)a * n;
+    const double *rb = L.data() + (size_t)b * n;
+    for (uint32_t y : live) {
+      if (y == a || y == b) continue;
+      const double v = std::min(ra[y], rb[y]);
+      ra[y] = v;
       L[(size_t)y * n + a] = v;
     }
     minr[a] = std::min(minr[a], minr[b]);
-    alive[b] = 0;
-    --live;
+    live.erase(std::lower_bound(live.begin(), live.end(), b));
+    for (uint32_t y = 0; y < n; ++y) {
+      L[(size_t)b * n + y] = NEG;
+      L[(size_t)y * n + b] = NEG;
+    }
     for (uint32_t i = 0; i < n; ++i)
       if (owner[i] == (int32_t)b) owner[i] = (int32_t)a;
-    recompute(a);
-    for (uint32_t x = 0; x < n; ++x) {
-      if (!alive[x] || x == a) continue;
-      if (best_of[x] == a || best_of[x] == b) {
-        recompute(x);
+    rescan(a);
+    for (uint32_t x : live) {
+      if (x == a) continue;
+      if (by[x] == a || by[x] == b) {
+        rescan(x);
       } else {
-        Key k = key(x, a);
-        if (key_less(k, best[x])) {
-          best[x] = k;
-          best_of[x] = a;
+        const double v = L[(size_t)x * n + a];
+        if (v >= tau && better(v, x, a, bs[x], x, by[x])) {
+          bs[x] = v;
+          by[x] = a;
         }
       }
     }
@@ -1056,8 +1065,7 @@ int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *i
   // label = position of the owning slot in the surviving list
   std::vector<int32_t> pos(n, -1);
   int32_t p = 0;
-  for (uint32_t x = 0; x < n; ++x)
-    if (alive[x]) pos[x] = p++;
+  for (uint32_t x : live) pos[x] = p++;
   for (uint32_t i = 0; i < n; ++i) label[i] = pos[owner[i]];
   return FS_OK;
 }

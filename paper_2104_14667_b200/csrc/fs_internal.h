@@ -58,6 +58,7 @@ struct OverlapArgs {
   uint64_t nbins;             // n_inputs + 1
   uint64_t n_inputs;
   const uint8_t *lut;         // grey LUT of nbins entries, or null (FP64 path)
+  int vec;                    // set by launch_overlap: outputs 16-B aligned
 };
 cudaError_t launch_overlap(const OverlapArgs &a, cudaStream_t s);
 

@@ -10,6 +10,7 @@
 //                                            real binarize + bit-pack kernel
 // Every kernel is a streaming HBM pass: 128-bit loads, coalesced stores, persistent
 // grids sized to the SM count, shared-memory privatised histograms.
+#include <algorithm>
 #include <cstdio>
 #include <cmath>
 
@@ -347,22 +348,30 @@ cudaError_t launch_pair_counts(const uint8_t *a, const uint8_t *b, uint64_t n,
 // Fused overlap pass over the tile-interleaved packed masks.
 //
 // A block owns 4 consecutive pixel tiles (4 warps, warp = tile, lane = word: 32 px).
-// TMA streams [4 tiles][16 masks][32 words] boxes (8 KB, contiguous in HBM) through a
-// 4-stage mbarrier ring; each thread folds its word of 16 masks into bit-sliced
-// Harley-Seal counters (ones/twos/fours/eights + ripple planes), so one 32-bit op
-// advances 32 pixels.  After the last mask the per-pixel counts are extracted,
-// transposed through SMEM and written lane-contiguously as counts / RGBA, and the
-// histogram is accumulated in SMEM with warp-aggregated atomics.
+// Lane 0 of warp 0 streams [4 tiles][16 masks][32 words] boxes (8 KB, contiguous in
+// HBM) through a 4-stage TMA ring (full/empty mbarriers, so warps drift up to a ring
+// apart instead of meeting at a block barrier per box).  Each thread folds its word of
+// 16 masks into bit-sliced Harley-Seal counters (ones/twos/fours/eights + NH ripple
+// planes): one 32-bit op advances 32 pixels.  After the tile's last mask the per-pixel
+// counts are extracted into registers and
+//   * the histogram is run-length encoded over the thread's 32 consecutive pixels
+//     (flood masks are spatially coherent: ~1-3 shared-memory atomics per word),
+//   * the counts are transposed through a padded SMEM tile with 16-B accesses
+//     (conflict-free) and written as 16-B streaming stores of counts and RGBA
+//     (RGBA from a per-block SMEM table of the exact FP64 grey levels).
+// Padding pixels past `pixels` (count 0) are counted once and removed from bin 0.
 // ---------------------------------------------------------------------------
 constexpr int kOvTiles = 4;
 constexpr int kOvThreads = 32 * kOvTiles;
 constexpr int kOvGroup = 16;
 constexpr int kOvStages = 4;
 constexpr int kOvStageWords = kOvTiles * kOvGroup * 32;  // 8 KB
-constexpr int kOvNH = 12;                                 // ripple planes (x16 masks)
-constexpr uint32_t kOvGroupsPerPass = (1u << kOvNH) - 1;
-constexpr size_t kOvSmem = (size_t)kOvStages * kOvStageWords * 4 + kHistSmemBins * 4 +
-                           kOvTiles * 32 * 33 * 4 + kOvStages * 8;
+constexpr int kOvTb = 36;                                 // transpose row stride (words)
+
+static size_t ov_smem_bytes(uint32_t sbins) {
+  return (size_t)kOvStages * kOvStageWords * 4 + (size_t)kOvTiles * 32 * kOvTb * 4 +
+         2 * kOvStages * 8 + 2 * (size_t)sbins * 4;
+}
 
 __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b,
                                     uint32_t c) {
@@ -371,13 +380,14 @@ __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32
   l = u ^ c;
 }
 
+template <int NH>
 struct HSCounter {
   uint32_t ones, twos, fours, eights;
-  uint32_t H[kOvNH];
+  uint32_t H[NH];
   __device__ __forceinline__ void reset() {
     ones = twos = fours = eights = 0;
 #pragma unroll
-    for (int i = 0; i < kOvNH; ++i) H[i] = 0;
+    for (int i = 0; i < NH; ++i) H[i] = 0;
   }
   __device__ __forceinline__ void add16(const uint32_t (&d)[16]) {
     uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
@@ -398,44 +408,57 @@ struct HSCounter {
     csa(sixteens, eights, eights, eightsA, eightsB);
     uint32_t carry = sixteens;
 #pragma unroll
-    for (int i = 0; i < kOvNH; ++i) {
+    for (int i = 0; i < NH; ++i) {
       const uint32_t t = H[i] & carry;
       H[i] ^= carry;
       carry = t;
     }
   }
-  // cnt[j] += wt * count(pixel j); ngroups bounds the ripple planes in use
-  __device__ __forceinline__ void extract(uint32_t (&cnt)[32], uint32_t wt, uint32_t ngroups) {
-    int nh = 0;
-    while (nh < kOvNH && (ngroups >> nh) != 0) ++nh;
+  // cnt[j] += wt * count(pixel j)
+  __device__ __forceinline__ void extract(uint32_t (&cnt)[32], uint32_t wt) const {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       uint32_t c = ((ones >> j) & 1u) | (((twos >> j) & 1u) << 1) |
                    (((fours >> j) & 1u) << 2) | (((eights >> j) & 1u) << 3);
 #pragma unroll
-      for (int i = 0; i < kOvNH; ++i)
-        if (i < nh) c += ((H[i] >> j) & 1u) << (4 + i);
+      for (int i = 0; i < NH; ++i) c |= ((H[i] >> j) & 1u) << (4 + i);
       cnt[j] += wt * c;
     }
   }
 };
 
+__device__ __forceinline__ void st_cs_v4(void *p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <bool GATHER, int NH>
 __global__ void __launch_bounds__(kOvThreads)
-    k_overlap(const __grid_constant__ CUtensorMap tm, const OverlapArgs a, int gather) {
+    k_overlap(const __grid_constant__ CUtensorMap tm, const OverlapArgs a, uint32_t sbins) {
+  constexpr uint32_t kPass = (1u << NH) - 1;  // 16-mask groups per extraction
   extern __shared__ __align__(128) uint8_t sm[];
   uint32_t *stage = reinterpret_cast<uint32_t *>(sm);
-  uint32_t *sh_hist = stage + kOvStages * kOvStageWords;
-  uint32_t(*tb)[32][33] = reinterpret_cast<uint32_t(*)[32][33]>(sh_hist + kHistSmemBins);
-  uint64_t *full = reinterpret_cast<uint64_t *>(sh_hist + kHistSmemBins + kOvTiles * 32 * 33);
+  uint32_t *tb = stage + kOvStages * kOvStageWords;
+  uint64_t *full = reinterpret_cast<uint64_t *>(tb + kOvTiles * 32 * kOvTb);
+  uint64_t *empty = full + kOvStages;
+  uint32_t *sh_hist = reinterpret_cast<uint32_t *>(empty + kOvStages);
+  uint32_t *sh_lut = sh_hist + sbins;
   const int tid = threadIdx.x;
   const int wi = tid >> 5, lane = tid & 31;
   const bool do_hist = a.bins != nullptr;
-  const bool sh_hist_on = do_hist && a.nbins <= kHistSmemBins;
-  if (sh_hist_on)
+  const bool hist_sh = do_hist && a.nbins <= sbins;
+  const bool lut_sh = a.rgba != nullptr && a.nbins <= sbins;
+  if (hist_sh)
     for (uint32_t i = tid; i < a.nbins; i += kOvThreads) sh_hist[i] = 0;
+  if (lut_sh)
+    for (uint32_t i = tid; i < a.nbins; i += kOvThreads) sh_lut[i] = rgba_word(i, a.n_inputs, a.lut);
   if (tid == 0) {
     ptx::prefetch_tmap(&tm);
-    for (int s = 0; s < kOvStages; ++s) ptx::mbar_init(&full[s], 1);
+    for (int s = 0; s < kOvStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], kOvTiles);
+    }
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -448,11 +471,8 @@ __global__ void __launch_bounds__(kOvThreads)
   const uint64_t nq = ntg > blockIdx.x ? (ntg - blockIdx.x - 1) / gridDim.x + 1 : 0;
   const uint64_t nitems = nq * GP;
 
-  // item -> (tile group, slot offset, mask count)
-  auto decode = [&](uint64_t i, uint64_t &tg, uint32_t &off, uint32_t &cnt, uint32_t &g) {
-    const uint64_t q = i / GP;
-    g = (uint32_t)(i % GP);
-    tg = blockIdx.x + q * gridDim.x;
+  // group g -> first row (slot-list offset) and row count
+  auto group = [&](uint32_t g, uint32_t &off, uint32_t &cnt) {
     if (g < G1) {
       off = g * kOvGroup;
       cnt = min((uint32_t)kOvGroup, a.k1 - off);
@@ -462,89 +482,191 @@ __global__ void __launch_bounds__(kOvThreads)
       cnt = min((uint32_t)kOvGroup, a.k2 - gi * kOvGroup);
     }
   };
-  auto issue = [&](uint64_t i) {
-    uint64_t tg;
-    uint32_t off, cnt, g;
-    decode(i, tg, off, cnt, g);
-    const int s = (int)(i % kOvStages);
+  // producer cursor (thread 0 only)
+  uint64_t pq = 0;
+  uint32_t pg = 0;
+  auto issue_next = [&](int s) {
+    uint32_t off, cnt;
+    group(pg, off, cnt);
+    const int tile0 = (int)((blockIdx.x + pq * gridDim.x) * kOvTiles);
     uint32_t *dst = stage + s * kOvStageWords;
-    if (!gather) {
+    if (!GATHER) {
       ptx::mbar_arrive_expect_tx(&full[s], kOvStageWords * 4);
-      ptx::tma_load_3d(dst, &tm, 0, (int)off, (int)(tg * kOvTiles), &full[s]);
+      ptx::tma_load_3d(dst, &tm, 0, (int)off, tile0, &full[s]);
     } else {
       ptx::mbar_arrive_expect_tx(&full[s], cnt * kOvTiles * 32 * 4);
       for (uint32_t j = 0; j < cnt; ++j)
-        ptx::tma_load_3d(dst + j * kOvTiles * 32, &tm, 0, (int)__ldg(a.slots + off + j),
-                         (int)(tg * kOvTiles), &full[s]);
+        ptx::tma_load_3d(dst + j * kOvTiles * 32, &tm, 0, (int)__ldg(a.slots + off + j), tile0,
+                         &full[s]);
+    }
+    if (++pg == GP) {
+      pg = 0;
+      ++pq;
     }
   };
   if (tid == 0)
-    for (uint64_t i = 0; i < nitems && i < (uint64_t)kOvStages; ++i) issue(i);
+    for (int s = 0; s < kOvStages && (uint64_t)s < nitems; ++s) issue_next(s);
 
-  HSCounter hc;
+  HSCounter<NH> hc;
   hc.reset();
   uint32_t cnt32[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) cnt32[j] = 0;
   uint32_t groups_in_pass = 0;
+  uint64_t q = 0;
+  uint32_t g = 0;
+  int s = 0;
+  uint32_t phase = 0;
+  const bool vec = a.vec != 0;
 
   for (uint64_t i = 0; i < nitems; ++i) {
-    const int s = (int)(i % kOvStages);
-    uint64_t tg;
-    uint32_t off, cnt, g;
-    decode(i, tg, off, cnt, g);
-    ptx::mbar_wait(&full[s], (uint32_t)((i / kOvStages) & 1));
+    uint32_t off, cnt;
+    group(g, off, cnt);
+    ptx::mbar_wait(&full[s], phase);
     const uint32_t *st = stage + s * kOvStageWords;
     uint32_t d[16];
+    if (cnt == (uint32_t)kOvGroup) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int idx = gather ? ((j * kOvTiles + wi) * 32 + lane) : ((wi * kOvGroup + j) * 32 + lane);
-      d[j] = (j < (int)cnt) ? st[idx] : 0u;
+      for (int j = 0; j < 16; ++j)
+        d[j] = GATHER ? st[(j * kOvTiles + wi) * 32 + lane] : st[(wi * kOvGroup + j) * 32 + lane];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t v =
+            GATHER ? st[(j * kOvTiles + wi) * 32 + lane] : st[(wi * kOvGroup + j) * 32 + lane];
+        d[j] = (j < (int)cnt) ? v : 0u;
+      }
     }
-    __syncthreads();  // every thread has read stage s
-    if (tid == 0 && i + kOvStages < nitems) issue(i + kOvStages);
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    if (tid == 0 && i + kOvStages < nitems) {
+      ptx::mbar_wait(&empty[s], phase);
+      issue_next(s);
+    }
     hc.add16(d);
     ++groups_in_pass;
     const bool range_end = (g == G1 - 1 && G1 > 0) || g == GP - 1;
-    if (range_end || groups_in_pass == kOvGroupsPerPass) {
-      hc.extract(cnt32, g < G1 ? a.w1 : a.w2, groups_in_pass);
+    if (range_end || groups_in_pass == kPass) {
+      hc.extract(cnt32, g < G1 ? a.w1 : a.w2);
       hc.reset();
       groups_in_pass = 0;
     }
     if (g == GP - 1) {
-      // epilogue for tile tg*4 + wi: transpose, then lane-contiguous stores
+      const uint64_t tile = (blockIdx.x + q * gridDim.x) * kOvTiles + wi;
+      if (tile < ntiles) {
+        if (do_hist) {
+          // run-length over this word's 32 consecutive pixels
+          uint32_t cur = cnt32[0], run = 1;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) tb[wi][lane][j] = cnt32[j];
-      __syncwarp();
-      const uint64_t wbase = (tg * kOvTiles + wi) * 32;
-      for (int r = 0; r < 32; ++r) {
-        const uint64_t px = (wbase + r) * 32 + lane;
-        const bool pv = px < a.pixels;
-        const uint32_t c = tb[wi][r][lane];
-        if (pv) {
-          if (a.counts) a.counts[px] = c;
-          if (a.rgba) a.rgba[px] = rgba_word(c, a.n_inputs, a.lut);
+          for (int j = 1; j < 32; ++j) {
+            const uint32_t c = cnt32[j];
+            if (c != cur) {
+              if (hist_sh)
+                atomicAdd(sh_hist + cur, run);
+              else if (cur < a.nbins)
+                atomicAdd(a.bins + cur, (unsigned long long)run);
+              cur = c;
+              run = 0;
+            }
+            ++run;
+          }
+          if (hist_sh)
+            atomicAdd(sh_hist + cur, run);
+          else if (cur < a.nbins)
+            atomicAdd(a.bins + cur, (unsigned long long)run);
         }
-        if (do_hist) hist_add(c, pv && c < a.nbins, sh_hist_on ? sh_hist : nullptr, a.bins);
+        if (a.counts != nullptr || a.rgba != nullptr) {
+          uint32_t *row = tb + (wi * 32 + lane) * kOvTb;
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            *reinterpret_cast<uint4 *>(row + 4 * v) =
+                make_uint4(cnt32[4 * v], cnt32[4 * v + 1], cnt32[4 * v + 2], cnt32[4 * v + 3]);
+          __syncwarp();
+          const uint64_t wbase = tile * 32;
+#pragma unroll 2
+          for (int it = 0; it < 8; ++it) {
+            const int w = it * 4 + (lane >> 3), b0 = (lane & 7) * 4;
+            const uint4 c = *reinterpret_cast<const uint4 *>(tb + (wi * 32 + w) * kOvTb + b0);
+            const uint64_t px0 = (wbase + w) * 32 + b0;
+            uint4 r = make_uint4(0, 0, 0, 0);
+            if (a.rgba != nullptr) {
+              if (lut_sh) {
+                r.x = sh_lut[c.x]; r.y = sh_lut[c.y]; r.z = sh_lut[c.z]; r.w = sh_lut[c.w];
+              } else {
+                r.x = rgba_word(c.x, a.n_inputs, a.lut);
+                r.y = rgba_word(c.y, a.n_inputs, a.lut);
+                r.z = rgba_word(c.z, a.n_inputs, a.lut);
+                r.w = rgba_word(c.w, a.n_inputs, a.lut);
+              }
+            }
+            if (vec && px0 + 4 <= a.pixels) {
+              if (a.counts) st_cs_v4(a.counts + px0, c);
+              if (a.rgba) st_cs_v4(a.rgba + px0, r);
+            } else {
+              const uint32_t cv[4] = {c.x, c.y, c.z, c.w}, rv[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (px0 + e < a.pixels) {
+                  if (a.counts) a.counts[px0 + e] = cv[e];
+                  if (a.rgba) a.rgba[px0 + e] = rv[e];
+                }
+            }
+          }
+          __syncwarp();
+        }
       }
-      __syncwarp();
 #pragma unroll
       for (int j = 0; j < 32; ++j) cnt32[j] = 0;
     }
+    if (++s == kOvStages) {
+      s = 0;
+      phase ^= 1u;
+    }
+    if (++g == GP) {
+      g = 0;
+      ++q;
+    }
   }
   __syncthreads();
-  if (sh_hist_on)
+  if (hist_sh)
     for (uint32_t i = tid; i < a.nbins; i += kOvThreads)
       if (sh_hist[i]) atomicAdd(a.bins + i, (unsigned long long)sh_hist[i]);
+  if (do_hist && blockIdx.x == 0 && tid == 0) {
+    // padding pixels of the last tile were counted in bin 0
+    const uint64_t pad = ntiles * 1024 - a.pixels;
+    if (pad) atomicAdd(a.bins, (unsigned long long)(0ull - pad));
+  }
 }
 
-cudaError_t launch_overlap(const OverlapArgs &a, cudaStream_t s) {
-  if (a.pixels == 0) return cudaSuccess;
+template <bool GATHER, int NH>
+static cudaError_t launch_overlap_t(const CUtensorMap &tm, const OverlapArgs &a, uint32_t sbins,
+                                    uint64_t ntg, cudaStream_t s) {
+  const size_t smem = ov_smem_bytes(sbins);
+  static size_t attr = 0;
+  if (attr < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_overlap<GATHER, NH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_overlap<GATHER, NH>, kOvThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = (uint64_t)num_sms() * per_sm;
+  if (grid > ntg) grid = ntg;
+  k_overlap<GATHER, NH><<<(unsigned)grid, kOvThreads, smem, s>>>(tm, a, sbins);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_overlap(const OverlapArgs &a_in, cudaStream_t s) {
+  if (a_in.pixels == 0) return cudaSuccess;
+  OverlapArgs a = a_in;
+  a.vec = ((reinterpret_cast<uintptr_t>(a.counts) | reinterpret_cast<uintptr_t>(a.rgba)) & 15) == 0;
   const uint32_t k = a.k1 + a.k2;
   const int64_t first = contiguous_run(a.host_slots, k);
   CUtensorMap tm;
   cudaError_t e;
-  const int gather = first < 0 ? 1 : 0;
+  const bool gather = first < 0;
   const uint64_t ntiles = a.wpm / 32;
   if (!gather)
     e = encode_packed_map(&tm, a.packed, a.capacity, (uint64_t)first, k, ntiles, 32, kOvGroup,
@@ -552,20 +674,19 @@ cudaError_t launch_overlap(const OverlapArgs &a, cudaStream_t s) {
   else
     e = encode_packed_map(&tm, a.packed, a.capacity, 0, a.capacity, ntiles, 32, 1, kOvTiles, 0);
   if (e != cudaSuccess) return e;
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(k_overlap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOvSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_overlap, kOvThreads, kOvSmem);
-  if (per_sm < 1) per_sm = 1;
+  // shared-memory histogram / RGBA table sized to the overlap classes
+  uint32_t sbins = 0;
+  if (a.nbins <= kHistSmemBins) sbins = (uint32_t)((a.nbins + 31) / 32 * 32);
   const uint64_t ntg = (ntiles + kOvTiles - 1) / kOvTiles;
-  uint64_t grid = (uint64_t)num_sms() * per_sm;
-  if (grid > ntg) grid = ntg;
-  k_overlap<<<(unsigned)grid, kOvThreads, kOvSmem, s>>>(tm, a, gather);
-  return cudaGetLastError();
+  const uint32_t gmax = std::max((a.k1 + kOvGroup - 1) / kOvGroup, (a.k2 + kOvGroup - 1) / kOvGroup);
+  if (gather) {
+    if (gmax <= 31) return launch_overlap_t<true, 5>(tm, a, sbins, ntg, s);
+    if (gmax <= 255) return launch_overlap_t<true, 8>(tm, a, sbins, ntg, s);
+    return launch_overlap_t<true, 12>(tm, a, sbins, ntg, s);
+  }
+  if (gmax <= 31) return launch_overlap_t<false, 5>(tm, a, sbins, ntg, s);
+  if (gmax <= 255) return launch_overlap_t<false, 8>(tm, a, sbins, ntg, s);
+  return launch_overlap_t<false, 12>(tm, a, sbins, ntg, s);
 }
 
 // Per-item streaming accumulate (run_stream's kernel[i]): counts += bits of one

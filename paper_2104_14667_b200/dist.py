@@ -95,83 +95,102 @@ class ShardedEnsemble:
         self.stream = torch.cuda.Stream(device=self.device)
         self.ens.use_stream(self.stream.cuda_stream)
         self.capacity = int(capacity)
-        self._bufs = {}
+        self._bufs: dict = {}
 
     def close(self) -> None:
         self.ens.close()
 
-    def _buffers(self, k: int, n_inputs: int):
+    def _make_buffers(self, k: int, n_inputs: int, maps: bool):
         import torch
 
-        key = (k, n_inputs)
-        if key not in self._bufs:
-            nb, total = partial_layout(k, n_inputs)
-            px = self.rows * self.width
-            self._bufs = {key: dict(
-                part=torch.empty(total, dtype=torch.int64, device=self.device),
-                counts=torch.empty(px, dtype=torch.int32, device=self.device),
-                rgba=torch.empty(px * 4, dtype=torch.uint8, device=self.device),
-                h_part=torch.empty(total, dtype=torch.int64).pin_memory(),
-                nb=nb)}
-        return self._bufs[key]
-
-    def recompute_device(self, slots, *, engine: str = "auto", cycles: int = 1,
-                         remainder: int = 0, counts: bool = True, rgba: bool = True):
-        """Enqueue one recompute on the ensemble stream; returns the device buffers.
-        Nothing is synchronised: the all-reduce is ordered after the kernels on the
-        same stream."""
-        import torch
-
-        sl = np.asarray(list(slots), dtype=np.uint32)
-        k = int(sl.size)
-        n_inputs = cycles * k + remainder
-        b = self._buffers(k, n_inputs)
-        nb = b["nb"]
-        part = b["part"]
-        self.ens.overlap(sl, cycles=cycles, remainder=remainder,
-                         out_counts=b["counts"].data_ptr() if counts else None,
-                         out_rgba=b["rgba"].data_ptr() if rgba else None,
-                         out_bins=part.data_ptr(), counts=counts, rgba=rgba,
-                         device_outputs=True)
-        self.ens.gram(sl, engine=engine, out=part.data_ptr() + nb * 8, device_outputs=True)
-        with torch.cuda.stream(self.stream):
-            allreduce_partials(part, self.group)
+        nb, total = partial_layout(k, n_inputs)
+        px = self.rows * self.width
+        b = dict(nb=nb, k=k,
+                 part=torch.empty(total, dtype=torch.int64, device=self.device),
+                 counts=torch.empty(px, dtype=torch.int32, device=self.device),
+                 rgba=torch.empty(px * 4, dtype=torch.uint8, device=self.device),
+                 h_part=torch.empty(total, dtype=torch.int64).pin_memory(),
+                 event=torch.cuda.Event())
+        if maps:
+            b["h_counts"] = torch.empty(px, dtype=torch.int32).pin_memory()
+            b["h_rgba"] = torch.empty(px * 4, dtype=torch.uint8).pin_memory()
         return b
 
-    def fetch(self, b, *, counts: bool = True, rgba: bool = True):
-        """D2H of the summed partials (and this band's maps) on the ensemble stream."""
+    def _enqueue(self, sl: np.ndarray, b, *, engine: str, cycles: int = 1, remainder: int = 0,
+                 maps_to_host: bool = False):
+        """Overlap + Gram into the bucketed buffer, one all-reduce, D2H of the partials
+        (and of this band's maps when asked), then an event — all on the ensemble
+        stream, nothing synchronised."""
         import torch
 
-        k2 = b["part"].numel() - b["nb"]
-        k = int(round(k2 ** 0.5))
+        part = b["part"]
+        self.ens.overlap(sl, cycles=cycles, remainder=remainder,
+                         out_counts=b["counts"].data_ptr(), out_rgba=b["rgba"].data_ptr(),
+                         out_bins=part.data_ptr(), device_outputs=True)
+        self.ens.gram(sl, engine=engine, out=part.data_ptr() + b["nb"] * 8, device_outputs=True)
         with torch.cuda.stream(self.stream):
-            b["h_part"].copy_(b["part"], non_blocking=True)
-            hc = hr = None
-            if counts:
-                hc = torch.empty(b["counts"].shape, dtype=torch.int32, pin_memory=True)
-                hc.copy_(b["counts"], non_blocking=True)
-            if rgba:
-                hr = torch.empty(b["rgba"].shape, dtype=torch.uint8, pin_memory=True)
-                hr.copy_(b["rgba"], non_blocking=True)
-        self.stream.synchronize()
-        part = b["h_part"].numpy()
-        bins = part[: b["nb"]].copy()
-        gram = part[b["nb"]:].reshape(k, k).copy()
-        c = hc.numpy().view(np.uint32).reshape(self.rows, self.width) if counts else None
-        r = hr.numpy().reshape(self.rows, self.width, 4) if rgba else None
-        return c, bins, r, gram
+            allreduce_partials(part, self.group)
+            b["h_part"].copy_(part, non_blocking=True)
+            if maps_to_host:
+                b["h_counts"].copy_(b["counts"], non_blocking=True)
+                b["h_rgba"].copy_(b["rgba"], non_blocking=True)
+            b["event"].record(self.stream)
 
-    def recompute(self, slots, *, tau: float = 0.8, engine: str = "auto", ids=None):
-        """Full recompute: band maps + global histogram, Gram, similarity, outliers and
-        clusters (identical on every rank)."""
+    def _finish(self, b, ids, tau: float, analytics: bool, maps_to_host: bool):
         from .analytics import cluster_from_similarity, outliers_from_similarity, similarity_from_gram
 
-        b = self.recompute_device(slots, engine=engine)
-        c, bins, r, gram = self.fetch(b)
-        sl = list(slots)
-        ids = ids or [f"s{i:04d}" for i in sl]
-        sim = similarity_from_gram(gram)
-        outl = outliers_from_similarity(sim, ids) if len(ids) >= 2 else None
-        clus = cluster_from_similarity(sim, ids, tau)
-        return {"counts": c, "bins": bins, "rgba": r, "gram": gram, "similarity": sim,
-                "outliers": outl, "clusters": clus}
+        b["event"].synchronize()
+        part = b["h_part"].numpy()
+        k = b["k"]
+        out = {"bins": part[: b["nb"]].copy(), "gram": part[b["nb"]:].reshape(k, k).copy()}
+        if maps_to_host:
+            # views of the pinned frame buffers: valid until this buffer's next frame
+            # (two frames later) is enqueued — copy them to keep them longer
+            out["counts"] = b["h_counts"].numpy().view(np.uint32).reshape(self.rows, self.width)
+            out["rgba"] = b["h_rgba"].numpy().reshape(self.rows, self.width, 4)
+        if analytics:
+            sim = similarity_from_gram(out["gram"])
+            out["similarity"] = sim
+            out["outliers"] = outliers_from_similarity(sim, ids) if len(ids) >= 2 else None
+            out["clusters"] = cluster_from_similarity(sim, ids, tau)
+        return out
+
+    def run_frames(self, slots, n_frames: int, *, tau: float = 0.8, engine: str = "auto",
+                   ids=None, maps_to_host: bool = False, analytics_ranks: str = "all",
+                   before_frame=None, keep: bool = True):
+        """``n_frames`` full recomputes of the working set, double-buffered: frame f+1's
+        device work (overlap, Gram, all-reduce, D2H) is enqueued before frame f's host
+        analytics (Jaccard, outliers, clusters) run, so the two overlap — the
+        interactive-recompute loop of service.py:143-175 at GPU rate.
+        ``before_frame(f)`` runs first in each frame (e.g. streaming new rasters in).
+        Returns the per-frame results (only the last one unless ``keep``)."""
+        sl = np.ascontiguousarray(np.asarray(list(slots), dtype=np.uint32))
+        k = int(sl.size)
+        ids = list(ids) if ids is not None else [f"s{i:04d}" for i in sl.tolist()]
+        key = (k, maps_to_host)
+        if self._bufs.get("key") != key:
+            self._bufs = {"key": key, "b": [self._make_buffers(k, k, maps_to_host) for _ in range(2)]}
+        bufs = self._bufs["b"]
+        # "all": every rank runs the host analytics; "root": rank 0 only; "none": skip
+        analytics = analytics_ranks == "all" or (analytics_ranks == "root" and self.rank == 0)
+        results, pending = [], None
+        for f in range(n_frames):
+            if before_frame is not None:
+                before_frame(f)
+            b = bufs[f % 2]
+            self._enqueue(sl, b, engine=engine, maps_to_host=maps_to_host)
+            if pending is not None:
+                r = self._finish(pending, ids, tau, analytics, maps_to_host)
+                if keep:
+                    results.append(r)
+            pending = b
+        if pending is not None:
+            results.append(self._finish(pending, ids, tau, analytics, maps_to_host))
+        return results if keep else results[-1:]
+
+    def recompute(self, slots, *, tau: float = 0.8, engine: str = "auto", ids=None):
+        """One full recompute: this band's counts/RGBA + the global histogram, Gram,
+        similarity, outliers and clusters (identical on every rank)."""
+        r = self.run_frames(slots, 1, tau=tau, engine=engine, ids=ids, maps_to_host=True)[0]
+        r["counts"], r["rgba"] = r["counts"].copy(), r["rgba"].copy()
+        return r

@@ -275,3 +275,37 @@ def test_c2_scale_properties():
     assert np.array_equal(r.reshape(-1, 4)[idx], want)
     sim = fs.similarity_from_gram(g_tc)
     assert np.array_equal(sim, O.similarity_from_gram(g_tc))
+
+
+# ---- sharded / pipelined recompute (single rank) ---------------------------------------
+
+def test_sharded_recompute_and_pipelined_frames():
+    """dist.ShardedEnsemble on one rank: recompute() and double-buffered run_frames()
+    reproduce the oracle's maps, histogram, Gram, outliers and clusters."""
+    from paper_2104_14667_b200.dist import ShardedEnsemble
+
+    w, h, k = 700, 333, 20
+    cells = [synth_cells(w, h, i, members=5, eps=0.04) for i in range(k)]
+    ids = [f"s{i:04d}" for i in range(k)]
+    counts = O.accumulate(cells, w, h)
+    g = O.gram(cells)
+    sim = O.similarity_from_gram(g)
+    sh = ShardedEnsemble(w, h, k)
+    try:
+        sh.ens.upload(cells)
+        r = sh.recompute(range(k), tau=0.8, ids=ids)
+        assert np.array_equal(r["counts"], counts)
+        assert np.array_equal(r["rgba"], O.composite(counts, k))
+        assert r["bins"].tolist() == O.overlap_counts(counts.reshape(-1), k).tolist()
+        assert np.array_equal(r["gram"], g)
+        assert r["clusters"] == O.cluster(sim, ids, 0.8)
+        assert r["outliers"] == O.outlier_scores(sim, ids)
+        frames = sh.run_frames(range(k), 5, tau=0.8, ids=ids, maps_to_host=True)
+        assert len(frames) == 5
+        for f in frames[-2:]:  # map views of the last two frames are still valid
+            assert np.array_equal(f["counts"], counts)
+        for f in frames:
+            assert np.array_equal(f["gram"], g)
+            assert f["clusters"] == O.cluster(sim, ids, 0.8)
+    finally:
+        sh.close()
