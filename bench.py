@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--tau", type=float, default=0.8)
-    ap.add_argument("--engine", default="tc", choices=["tc", "popc"])
+    ap.add_argument("--engine", default="tc-f4", choices=["tc-f4", "tc", "popc"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -505,7 +505,7 @@ def main():
             "gpu_launches": None,
         }
         # our kernels per resident step: fused overlap (1) + Gram
-        if args.engine == "tc":
+        if args.engine in ("tc", "tc-f4"):
             npanels = -(-k // (128 if k <= 128 else 256))
             gram_launches = 1 + (1 if npanels > 1 else 0) + 1  # diag, off-diag, reduce
         else:

@@ -53,6 +53,8 @@ extern "C" {
 #define FS_GRAM_AUTO 0
 #define FS_GRAM_POPC 1   /* CUDA-core AND+POPC on bit-packed masks           */
 #define FS_GRAM_TC_I8 2  /* tcgen05 kind::i8, bits expanded to u8 in SMEM    */
+#define FS_GRAM_TC_F4 3  /* diagonal tiles on tcgen05 kind::mxf4 (e2m1, scale 1, f32 exact
+                            per <= 2^24-px chunk), off-diagonal tiles on kind::i8 */
 
 /* ---- housekeeping ------------------------------------------------------ */
 const char *fs_last_error(void);

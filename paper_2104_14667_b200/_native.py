@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libfloodstream.so"
 
 FS_OK, FS_EINVAL, FS_ECUDA, FS_ENOMEM, FS_ENODEV = 0, 1, 2, 3, 4
 VARIANT_CODES = {"1b-initial": 0, "2b-initial": 1, "1b-final": 2, "2b-final": 3}
-GRAM_AUTO, GRAM_POPC, GRAM_TC_I8 = 0, 1, 2
+GRAM_AUTO, GRAM_POPC, GRAM_TC_I8, GRAM_TC_F4 = 0, 1, 2, 3
 KERNEL_PACK, KERNEL_OVERLAP, KERNEL_GRAM = 0, 1, 2
 
 

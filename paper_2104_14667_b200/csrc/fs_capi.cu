@@ -257,7 +257,7 @@ int fs_synchronize(void) {
   return FS_OK;
 }
 int fs_set_gram_engine(int engine) {
-  if (engine != FS_GRAM_POPC && engine != FS_GRAM_TC_I8)
+  if (engine != FS_GRAM_POPC && engine != FS_GRAM_TC_I8 && engine != FS_GRAM_TC_F4)
     return set_err(FS_EINVAL, "unknown gram engine");
   g_gram_engine = engine;
   return FS_OK;
@@ -803,8 +803,9 @@ int fs_ensemble_gram(fs_ensemble *e, const uint32_t *slots, uint32_t k, int engi
   if (k == 0) return FS_OK;
   if (!slots) return set_err(FS_EINVAL, "null slots");
   if (engine == FS_GRAM_AUTO) engine = g_gram_engine.load();
-  if (engine != FS_GRAM_POPC && engine != FS_GRAM_TC_I8)
+  if (engine != FS_GRAM_POPC && engine != FS_GRAM_TC_I8 && engine != FS_GRAM_TC_F4)
     return set_err(FS_EINVAL, "unknown gram engine");
+  const bool fp4 = engine == FS_GRAM_TC_F4;
   std::lock_guard<std::mutex> g(e->mu);
   DeviceGuard dg(e->device);
   int rc = upload_slots(e, slots, k);
@@ -823,14 +824,14 @@ int fs_ensemble_gram(fs_ensemble *e, const uint32_t *slots, uint32_t k, int engi
     CK(cudaMemsetAsync(gd, 0, gbytes, e->sk));
     CK(launch_gram_popc(e->packed, e->capacity, e->wpm, e->slots.as<uint32_t>(), k, gd, e->sk));
   } else {
-    CK(e->ws.ensure(gram_tc_workspace_bytes(k, e->wpm, e->num_sms)));
+    CK(e->ws.ensure(gram_tc_workspace_bytes(k, e->wpm, e->num_sms, fp4)));
     void *gws = nullptr;
     if (contiguous_run(slots, k) < 0) {
       CK(e->gather.ensure(gram_tc_gather_bytes(k, e->wpm)));
       gws = e->gather.p;
     }
     CK(launch_gram_tc(e->packed, e->capacity, e->wpm, e->slots.as<uint32_t>(), slots, k, gd,
-                      e->ws.p, gws, e->num_sms, e->sk));
+                      e->ws.p, gws, e->num_sms, fp4, e->sk));
   }
   rc = record_kernel(e, FS_KERNEL_GRAM, false);
   if (rc) return rc;

@@ -18,6 +18,13 @@
 //  * PANEL = 256: two M=128 halves.  Diagonal tiles issue half 0 with N=256 and half 1
 //    with N=128 (columns 128..255) — the lower-left quadrant is the transpose of the
 //    upper-right one and is mirrored by the reduce kernel (3/4 of the full work).
+//  * FP4 variant (diagonal tiles): tcgen05.mma.kind::mxf4.block_scale (e2m1 operands,
+//    every UE8M0 block scale = 1.0, f32 accumulators), twice the int8 MMA rate.  A wet
+//    bit becomes the e2m1 code 0b0010 (= 1.0), so products are exact 0/1 and the f32
+//    sums are exact integers while a CTA's K chunk stays <= 2^24 px.  Because a Gram
+//    entry is invariant under any permutation of the pixel (K) axis applied to both
+//    operands, the expander does not keep pixel order: nibble q of output word j is bit
+//    4q + j of the packed word, i.e. out_j = (w >> j-1) & 0x22222222 — two ops per 8 px.
 //  * Pixels (K) are split over CTAs; each CTA writes an int32 partial tile and a reduce
 //    kernel sums partials into the exact int64 Gram.  Partials are exact: a CTA's K
 //    range is far below 2^31 pixels.
@@ -30,7 +37,6 @@ namespace fs {
 namespace tc {
 
 constexpr int kThreads = 192;  // w0: TMEM alloc + MMA; w1..4: expanders + epilogue; w5: TMA
-constexpr int kStagePx = 128;  // K per operand stage: one 128-B SW128 row per mask
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kRawDepth = 2;
 
@@ -57,6 +63,31 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, 
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+// block-scaled descriptor (cute::UMMA::InstrDescriptorBlockScaled): a/b format E2M1 (1)
+// at bits 7/10, N>>3 at 17, scale format UE8M0 at 23, M>>4 at 24, sf ids 0, K = 64.
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accum, uint32_t sfa, uint32_t sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;"
+      "\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb));
+}
+
+// 16 columns of this warp's 32 TMEM lanes <- v
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
@@ -123,29 +154,53 @@ __device__ __forceinline__ void expand_row(uint32_t base, uint32_t row, uint4 v)
   }
 }
 
-template <int PANEL, bool DIAG>
+// FP4: one raw 16-B chunk (4 words, 128 px) of row `row` -> 4 operand chunks (64 B)
+// at chunk positions c0..c0+3 of SW128 row `row`.
+__device__ __forceinline__ void expand_row_f4(uint32_t base, uint32_t row, uint32_t c0, uint4 v) {
+  const uint32_t rbase = base + row * 128u;
+  const uint32_t sw = row & 7u;
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t x = w[q];
+    uint4 o;
+    o.x = (x << 1) & 0x22222222u;
+    o.y = x & 0x22222222u;
+    o.z = (x >> 1) & 0x22222222u;
+    o.w = (x >> 2) & 0x22222222u;
+    st_shared_v4(rbase + (((c0 + (uint32_t)q) ^ sw) << 4), o);
+  }
+}
+
+constexpr uint32_t kSfCol = 448;          // FP4: scale-factor columns [448, 480) of TMEM
+constexpr uint32_t kSfOnes = 0x7F7F7F7Fu; // UE8M0 127 = 2^0 in every byte
+constexpr uint64_t kF4MaxChunkPx = 1ull << 24;  // f32 sums stay exact below this
+
+template <int PANEL, bool DIAG, bool FP4 = false>
 struct Cfg {
   static constexpr int kRowsPerThread = PANEL / 128;  // per region, 128 expander threads
   static constexpr int kRegions = DIAG ? 1 : 2;
   static constexpr int kRawRow = (PANEL == 256 && !DIAG) ? 64 : 128;  // raw bytes/row/unit
-  static constexpr int kStagesPerUnit = kRawRow / 16;
+  static constexpr int kRawPerStage = FP4 ? 32 : 16;  // raw bytes per row per K stage
+  static constexpr int kStagesPerUnit = kRawRow / kRawPerStage;
   static constexpr int kRawUnitBytes = kRegions * PANEL * kRawRow;
   static constexpr int kRegionBytes = PANEL * 128;
   static constexpr int kStageBytes = kRegionBytes * kRegions;
   static constexpr int kStagesFit = (kSmemBudget - kRawDepth * kRawUnitBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   static constexpr int kHalves = PANEL / 128;
-  static constexpr uint32_t kTmemCols = PANEL == 256 ? 512u : 128u;
+  static constexpr uint32_t kTmemCols = (PANEL == 256 || FP4) ? 512u : 128u;
+  static_assert(!FP4 || DIAG, "FP4 path is for diagonal tiles (off-diagonal accumulators fill TMEM)");
   static constexpr int kSmemBytes =
       kRawDepth * kRawUnitBytes + kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(kStages >= 2, "operand ring too shallow");
 };
 
-template <int PANEL, bool DIAG>
+template <int PANEL, bool DIAG, bool FP4>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gram_tc(const __grid_constant__ CUtensorMap tm, uint32_t npanels, uint32_t kchunks,
               uint64_t units_per_chunk, uint64_t total_units, int32_t *__restrict__ partial) {
-  using C = Cfg<PANEL, DIAG>;
+  using C = Cfg<PANEL, DIAG, FP4>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   const uint32_t pad = (1024u - (raw_addr & 1023u)) & 1023u;
@@ -207,12 +262,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (FP4) {
+    // all block scales = 1.0: SFA / SFB columns [kSfCol, kSfCol + 32), every lane
+    if (warp >= 1 && warp <= 4) {
+      const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
+      tmem_st16(tmem + lanes + kSfCol, kSfOnes);
+      tmem_st16(tmem + lanes + kSfCol + 16, kSfOnes);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+  }
 
   if (warp == 0) {
     // ===== MMA issuer =====
     if (lane == 0 && nst > 0) {
-      constexpr uint32_t idA = idesc_i8(128, PANEL);
-      constexpr uint32_t idB = idesc_i8(128, 128);
+      constexpr uint32_t idA = FP4 ? idesc_mxf4(128, PANEL) : idesc_i8(128, PANEL);
+      constexpr uint32_t idB = FP4 ? idesc_mxf4(128, 128) : idesc_i8(128, 128);
+      const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 16;
       for (int j = 0; j < nst; ++j) {
         const int s = j % C::kStages;
         ptx::mbar_wait(&full[s], (uint32_t)((j / C::kStages) & 1));
@@ -220,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t a_base = op_base + s * C::kStageBytes;
         const uint32_t b_base = DIAG ? a_base : a_base + C::kRegionBytes;
 #pragma unroll
-        for (int ks = 0; ks < kStagePx / 32; ++ks) {
+        for (int ks = 0; ks < 4; ++ks) {  // 4 MMAs of 32 B of K per 128-B operand row
           const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
 #pragma unroll
           for (int h = 0; h < C::kHalves; ++h) {
@@ -228,10 +296,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (DIAG && PANEL == 256 && h == 1) {
               // rows 128..255 x cols 128..255 only
               const uint64_t bdesc = sw128_desc(b_base + 128 * 128 + ks * 32);
-              mma_i8(tmem + 256u, adesc, bdesc, idB, acc);
+              if (FP4)
+                mma_mxf4(tmem + 256u, adesc, bdesc, idB, acc, sfa, sfb);
+              else
+                mma_i8(tmem + 256u, adesc, bdesc, idB, acc);
             } else {
               const uint64_t bdesc = sw128_desc(b_base + ks * 32);
-              mma_i8(tmem + (uint32_t)(h * PANEL), adesc, bdesc, idA, acc);
+              if (FP4)
+                mma_mxf4(tmem + (uint32_t)(h * PANEL), adesc, bdesc, idA, acc, sfa, sfb);
+              else
+                mma_i8(tmem + (uint32_t)(h * PANEL), adesc, bdesc, idA, acc);
             }
           }
         }
@@ -278,9 +352,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int m = 0; m < C::kRowsPerThread; ++m) {
           const uint32_t rr = ptid + m * 128;
           const uint32_t sw = C::kRawRow == 128 ? (rr & 7u) : ((rr >> 1) & 3u);
-          const uint4 v = ld_shared_v4(rbase + r * PANEL * C::kRawRow + rr * C::kRawRow +
-                                       (((uint32_t)sub ^ sw) << 4));
-          expand_row(sbase + r * C::kRegionBytes, rr, v);
+          const uint32_t rrow = rbase + r * PANEL * C::kRawRow + rr * C::kRawRow;
+          if (FP4) {
+            // 32 raw bytes (256 px) -> the whole 128-B operand row
+#pragma unroll
+            for (int hch = 0; hch < 2; ++hch) {
+              const uint32_t u = (uint32_t)(2 * sub + hch);
+              const uint4 v = ld_shared_v4(rrow + ((u ^ sw) << 4));
+              expand_row_f4(sbase + r * C::kRegionBytes, rr, 4u * hch, v);
+            }
+          } else {
+            const uint4 v = ld_shared_v4(rrow + (((uint32_t)sub ^ sw) << 4));
+            expand_row(sbase + r * C::kRegionBytes, rr, v);
+          }
         }
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&full[s]);
@@ -306,6 +390,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (nst == 0) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = 0;
+        } else if (FP4) {  // exact integer-valued f32 -> int32
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = (uint32_t)__float2int_rn(__uint_as_float(v[e]));
         }
         int4 *dst = reinterpret_cast<int4 *>(out + (uint64_t)row * PANEL + c0);
 #pragma unroll
@@ -391,7 +478,7 @@ struct Plan {
 };
 
 static void chunking(uint64_t total_units, uint32_t ntiles, int num_sms, uint32_t &kc,
-                     uint64_t &upc) {
+                     uint64_t &upc, uint64_t max_upc = UINT64_MAX) {
   if (ntiles == 0 || total_units == 0) {
     kc = 0;
     upc = 0;
@@ -401,10 +488,11 @@ static void chunking(uint64_t total_units, uint32_t ntiles, int num_sms, uint32_
   if (want < 1) want = 1;
   if (want > total_units) want = total_units;
   upc = (total_units + want - 1) / want;
+  if (upc > max_upc) upc = max_upc;
   kc = (uint32_t)((total_units + upc - 1) / upc);
 }
 
-static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms) {
+static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms, bool fp4) {
   Plan p{};
   p.panel = k <= 128 ? 128 : 256;
   p.npanels = (k + p.panel - 1) / p.panel;
@@ -413,23 +501,25 @@ static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms) {
   const uint64_t ntiles = wpm / 32;
   p.units_diag = ntiles;  // diag tiles: one 128-B raw row per tile
   p.units_off = p.panel == 256 ? ntiles * 2 : ntiles;  // 256-panel off-diag: 64-B halves
-  chunking(p.units_diag, p.ndiag, num_sms, p.kc_diag, p.upc_diag);
+  // FP4 diagonal tiles accumulate in f32: a chunk (unit = 1024 px) must stay <= 2^24 px
+  chunking(p.units_diag, p.ndiag, num_sms, p.kc_diag, p.upc_diag,
+           fp4 ? kF4MaxChunkPx / 1024 : UINT64_MAX);
   chunking(p.units_off, p.noff, num_sms, p.kc_off, p.upc_off);
   return p;
 }
 
 }  // namespace tc
 
-size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms) {
-  tc::Plan p = tc::make_plan(k, wpm, num_sms);
+size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms, bool fp4) {
+  tc::Plan p = tc::make_plan(k, wpm, num_sms, fp4);
   const uint64_t per_tile = (uint64_t)p.panel * p.panel * 4;
   return (size_t)(((uint64_t)p.ndiag * p.kc_diag + (uint64_t)p.noff * p.kc_off) * per_tile);
 }
 
-template <int PANEL, bool DIAG>
+template <int PANEL, bool DIAG, bool FP4 = false>
 static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t *part,
                               cudaStream_t s) {
-  using C = tc::Cfg<PANEL, DIAG>;
+  using C = tc::Cfg<PANEL, DIAG, FP4>;
   const uint32_t ntiles = DIAG ? p.ndiag : p.noff;
   const uint32_t kc = DIAG ? p.kc_diag : p.kc_off;
   const uint64_t upc = DIAG ? p.upc_diag : p.upc_off;
@@ -437,13 +527,13 @@ static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t 
   if (ntiles == 0 || kc == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<PANEL, DIAG>,
+    cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<PANEL, DIAG, FP4>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  tc::k_gram_tc<PANEL, DIAG><<<ntiles * kc, tc::kThreads, C::kSmemBytes, s>>>(
+  tc::k_gram_tc<PANEL, DIAG, FP4><<<ntiles * kc, tc::kThreads, C::kSmemBytes, s>>>(
       tm, p.npanels, kc, upc, units, part);
   return cudaGetLastError();
 }
@@ -453,9 +543,9 @@ size_t gram_tc_gather_bytes(uint32_t k, uint64_t wpm) { return (size_t)k * wpm *
 cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t wpm,
                            const uint32_t *slots, const uint32_t *host_slots, uint32_t k,
                            unsigned long long *gram, void *workspace, void *gather_ws,
-                           int num_sms, cudaStream_t s) {
+                           int num_sms, bool fp4, cudaStream_t s) {
   if (k == 0) return cudaSuccess;
-  tc::Plan p = tc::make_plan(k, wpm, num_sms);
+  tc::Plan p = tc::make_plan(k, wpm, num_sms, fp4);
   const uint64_t ntiles = wpm / 32;
   // contiguous slot run -> map straight over the ensemble; else gather first
   const uint32_t *src = packed;
@@ -487,10 +577,14 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
                              raw_off == 16 ? 64 : 128)) != cudaSuccess)
     return e;
   if (p.panel == 128) {
-    if ((e = launch_one<128, true>(tm_diag, p, part_diag, s)) != cudaSuccess) return e;
+    e = fp4 ? launch_one<128, true, true>(tm_diag, p, part_diag, s)
+            : launch_one<128, true>(tm_diag, p, part_diag, s);
+    if (e != cudaSuccess) return e;
     if ((e = launch_one<128, false>(tm_off, p, part_off, s)) != cudaSuccess) return e;
   } else {
-    if ((e = launch_one<256, true>(tm_diag, p, part_diag, s)) != cudaSuccess) return e;
+    e = fp4 ? launch_one<256, true, true>(tm_diag, p, part_diag, s)
+            : launch_one<256, true>(tm_diag, p, part_diag, s);
+    if (e != cudaSuccess) return e;
     if ((e = launch_one<256, false>(tm_off, p, part_off, s)) != cudaSuccess) return e;
   }
   const uint64_t total = (uint64_t)(p.ndiag + p.noff) * per_tile;

@@ -69,13 +69,14 @@ cudaError_t launch_gram_popc(const uint32_t *packed, uint64_t capacity, uint64_t
                              const uint32_t *slots, uint32_t k, unsigned long long *gram,
                              cudaStream_t s);
 // tcgen05 kind::i8 Gram; partial workspace sized by gram_tc_workspace_bytes().
-size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms);
+// fp4: diagonal tiles on kind::mxf4 (off-diagonal tiles stay on kind::i8).
+size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms, bool fp4);
 // Non-contiguous slot lists are first gathered into gather_ws (gram_tc_gather_bytes).
 size_t gram_tc_gather_bytes(uint32_t k, uint64_t wpm);
 cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t wpm,
                            const uint32_t *slots, const uint32_t *host_slots, uint32_t k,
                            unsigned long long *gram, void *workspace, void *gather_ws,
-                           int num_sms, cudaStream_t s);
+                           int num_sms, bool fp4, cudaStream_t s);
 // gram (k x k, upper tiles filled) -> symmetric
 cudaError_t launch_gram_mirror(unsigned long long *gram, uint32_t k, uint32_t tile,
                                cudaStream_t s);

@@ -33,7 +33,8 @@ from .analytics import (
     similarity_from_gram,
 )
 
-_GRAM_ENGINES = {"auto": N.GRAM_AUTO, "popc": N.GRAM_POPC, "tc": N.GRAM_TC_I8, "tc-i8": N.GRAM_TC_I8}
+_GRAM_ENGINES = {"auto": N.GRAM_AUTO, "popc": N.GRAM_POPC, "tc": N.GRAM_TC_I8, "tc-i8": N.GRAM_TC_I8,
+                 "tc-f4": N.GRAM_TC_F4}
 
 
 @dataclass

@@ -167,7 +167,7 @@ def test_ensemble_cycled_overlap(golden, case):
 
 # ---- Gram engines ----------------------------------------------------------------------
 
-@pytest.mark.parametrize("engine", ["popc", "tc"])
+@pytest.mark.parametrize("engine", ["popc", "tc", "tc-f4"])
 @pytest.mark.parametrize("k,h,w", [(1, 3, 5), (2, 1, 1), (16, 64, 64), (31, 17, 129),
                                    (128, 32, 32), (129, 40, 33), (200, 64, 80),
                                    (256, 32, 64), (257, 16, 33), (300, 24, 40)])
@@ -187,7 +187,7 @@ def test_gram_engines_exact(engine, k, h, w):
     assert np.array_equal(got_p, want[np.ix_(perm, perm)])
 
 
-@pytest.mark.parametrize("engine", ["popc", "tc"])
+@pytest.mark.parametrize("engine", ["popc", "tc", "tc-f4"])
 def test_gram_large_pixels(engine):
     """Many K stages and K chunks: 24 flood-like masks of 1536 x 1100 px."""
     cells = [synth_cells(1100, 1536, i, members=6, eps=0.05) for i in range(24)]
@@ -264,7 +264,9 @@ def test_c2_scale_properties():
         c, b, r = ens.overlap()
         g_tc = ens.gram(engine="tc")
         g_pc = ens.gram(engine="popc")
+        g_f4 = ens.gram(engine="tc-f4")
     assert np.array_equal(g_tc, g_pc)
+    assert np.array_equal(g_f4, g_pc)
     assert int(b.sum()) == w * h
     assert int(c.sum(dtype=np.uint64)) == int(np.trace(g_tc))
     assert np.array_equal(b, np.bincount(c.reshape(-1), minlength=k + 1))
@@ -309,3 +311,18 @@ def test_sharded_recompute_and_pipelined_frames():
             assert f["clusters"] == O.cluster(sim, ids, 0.8)
     finally:
         sh.close()
+
+
+def test_gram_f4_chunk_cap_large_k_range():
+    """FP4 accumulates in f32: a K chunk is capped at 2^24 px.  One 128-panel of 3 masks
+    over 40 Mpx forces several capped chunks per CTA grid; all-ones masks make the
+    diagonal entries as large as possible."""
+    w, h = 8192, 5000
+    cells = [np.ones((h, w), np.uint8), synth_cells(w, h, 1, members=2, eps=0.3),
+             np.zeros((h, w), np.uint8)]
+    with DeviceEnsemble(w, h, 3) as ens:
+        ens.upload(cells)
+        got = ens.gram(engine="tc-f4")
+        ref = ens.gram(engine="popc")
+    assert np.array_equal(got, ref)
+    assert got[0, 0] == w * h
