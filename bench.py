@@ -363,13 +363,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    kern = {"overlap": [], "gram": []}
+    kern = {"overlap": [], "gram": [], "recompute": []}
 
     def sample_kernels(_f):
-        # per-kernel CUDA-event durations of the previous frame (ensemble stream)
+        # CUDA-event duration of the previous frame's recompute call (ensemble stream)
         if _f > 0:
-            kern["overlap"].append(ens.kernel_ms("overlap"))
-            kern["gram"].append(ens.kernel_ms("gram"))
+            kern["recompute"].append(ens.kernel_ms("recompute"))
 
     # ---- resident timed region: K pipelined full recomputes ---------------------------
     sh.run_frames(slots, args.warmup, tau=args.tau, engine=args.engine, ids=ids,
@@ -409,6 +408,22 @@ def main():
     sh.run_frames(slots, 6, tau=args.tau, engine=args.engine, ids=ids, analytics_ranks="none",
                   keep=False, before_frame=sample_kernels)
     sample_kernels(1)
+    fused = None
+    # the two stages as separate kernels (the unfused path), for the breakdown
+    d_c = torch.empty(P_band, dtype=torch.int32, device=dev)
+    d_r = torch.empty(P_band * 4, dtype=torch.uint8, device=dev)
+    d_b = torch.empty(k + 1, dtype=torch.int64, device=dev)
+    d_g = torch.empty(k * k, dtype=torch.int64, device=dev)
+    for _ in range(6):
+        ens.overlap(slots, out_counts=d_c.data_ptr(), out_rgba=d_r.data_ptr(),
+                    out_bins=d_b.data_ptr(), device_outputs=True)
+        kern["overlap"].append(ens.kernel_ms("overlap"))
+        ens.gram(slots, engine=args.engine, out=d_g.data_ptr(), device_outputs=True)
+        kern["gram"].append(ens.kernel_ms("gram"))
+        fused = ens.products(slots, engine=args.engine, out_counts=d_c.data_ptr(),
+                             out_rgba=d_r.data_ptr(), out_bins=d_b.data_ptr(),
+                             out_gram=d_g.data_ptr(), device_outputs=True)[4]
+    del d_c, d_r, d_b, d_g
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     traffic = load_traffic()
@@ -416,20 +431,37 @@ def main():
     gr_ms = statistics.median(kern["gram"])
     ov_bytes = k * P_band / 8 + 4 * P_band + 4 * P_band + 8 * (k + 1)
     gram_ops = float(k) * (k + 1) * P_band  # upper triangle incl. diagonal, MAC = 2 ops
-    i8_peak = 4500.0  # dense int8 tcgen05, TOPS (B200_PROFILING.md fallback table)
+    # dense tensor peaks (B200_PROFILING.md fallback table; MEASURED_PEAKS.json has bf16 only)
+    t_peak, t_kind = {"tc-f4": (9000.0, "fp4 (kind::mxf4) 9 PFLOP/s dense"),
+                      "tc": (4500.0, "int8 (kind::i8) 4.5 POPS dense"),
+                      "popc": (4500.0, "int8 4.5 POPS dense (CUDA-core engine, for scale)")}[args.engine]
     rl_over = {"bound": "hbm", "achieved": round(ov_bytes / ov_ms / 1e6, 1), "peak": hbm,
                "unit": "GB/s", "frac": round(ov_bytes / ov_ms / 1e6 / hbm, 4),
                "traffic": traffic.get("k_overlap"), "kernel_ms": round(ov_ms, 4),
                "bytes_per_launch": int(ov_bytes),
                "bytes_def": "N*P/8 packed read + 4P counts + 4P RGBA + 8(N+1) bins",
                "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy test)"}
-    rl_gram = {"bound": "tensor", "achieved": round(gram_ops / gr_ms / 1e9, 1), "peak": i8_peak,
-               "unit": "TFLOP/s", "frac": round(gram_ops / gr_ms / 1e9 / i8_peak, 4),
-               "traffic": traffic.get("k_gram_tc"), "kernel_ms": round(gr_ms, 4),
-               "ops_per_launch": gram_ops,
-               "ops_def": "N(N+1)*P = 2 ops x the N(N+1)/2 distinct mask pairs x P px",
-               "peak_note": "dense int8 4.5 POPS (no measured int8 peak in MEASURED_PEAKS.json)"}
-    dominant = rl_gram if gr_ms >= ov_ms else rl_over
+    rl_gram = {"bound": "tensor", "achieved": round(gram_ops / gr_ms / 1e9, 1), "peak": t_peak,
+               "unit": "TFLOP/s", "frac": round(gram_ops / gr_ms / 1e9 / t_peak, 4),
+               "traffic": traffic.get("k_gram_tc_f4" if args.engine == "tc-f4" else "k_gram_tc"),
+               "kernel_ms": round(gr_ms, 4), "ops_per_launch": gram_ops,
+               "ops_def": "N(N+1)*P = 2 ops x the N(N+1)/2 distinct mask pairs x P px "
+                          "(the kernel issues 3/4 N^2 P MACs: 128-row MMA granularity)",
+               "peak_note": t_kind}
+    rc_ms = statistics.median(kern["recompute"])
+    rl_fused = {"bound": "tensor", "kernel": "k_gram_tc<...,FUSE> + k_gram_reduce" if fused
+                else "k_overlap + k_gram_tc + k_gram_reduce",
+                "fused": bool(fused), "achieved": round(gram_ops / rc_ms / 1e9, 1),
+                "peak": t_peak, "unit": "TFLOP/s",
+                "frac": round(gram_ops / rc_ms / 1e9 / t_peak, 4),
+                "traffic": traffic.get("k_gram_tc_fused") if fused else None,
+                "kernel_ms": round(rc_ms, 4), "ops_per_launch": gram_ops,
+                "ops_def": rl_gram["ops_def"], "peak_note": t_kind,
+                "hbm_achieved_gbs": round(ov_bytes / rc_ms / 1e6, 1),
+                "hbm_frac": round(ov_bytes / rc_ms / 1e6 / hbm, 4),
+                "hbm_bytes_def": "same algorithmic bytes as the overlap pass (the Gram reads "
+                                 "the same packed tiles)"}
+    dominant = rl_fused
 
     # ---- end-to-end through the public API from pinned host rasters --------------------
     e2e = None
@@ -498,7 +530,7 @@ def main():
             "host_analytics_ms": round(statistics.median(host_ms), 4) if host_ms else None,
             "clusters": n_clusters if host_ms else None,
             "roofline": dominant,
-            "kernels": {"overlap": rl_over, "gram": rl_gram},
+            "kernels": {"recompute": rl_fused, "overlap": rl_over, "gram": rl_gram},
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -510,7 +542,8 @@ def main():
             gram_launches = 1 + (1 if npanels > 1 else 0) + 1  # diag, off-diag, reduce
         else:
             gram_launches = 1 + (1 if k > 64 else 0)  # popc, mirror
-        line["gpu_launches"] = (1 + gram_launches) * args.steps
+        # + the overlap kernel unless fused into the diagonal Gram CTAs
+        line["gpu_launches"] = (gram_launches + (0 if fused else 1)) * args.steps
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
     sh.close()

@@ -128,12 +128,23 @@ int fs_ensemble_running_counts(fs_ensemble *ens, uint32_t *counts, int64_t *bins
 /* Pairwise intersection counts over slots: gram[i*k+j] int64 (host or device). */
 int fs_ensemble_gram(fs_ensemble *ens, const uint32_t *slots, uint32_t k, int engine,
                      int64_t *gram, int device_outputs);
+/* One full recompute of the working set (service.py:143-175 + the /clusters and
+ * /outliers Gram, analytics.py:106-181): counts, histogram (k+1 bins), composite and
+ * Gram over slots[0..k), weights 1.  With a tensor-core engine and k <= 256 the
+ * overlap products come out of the Gram's diagonal CTAs (one HBM read of the packed
+ * masks for everything; *fused = 1), else from the separate overlap kernel.  Any
+ * output may be NULL (gram NULL: overlap only).                                     */
+int fs_ensemble_recompute(fs_ensemble *ens, const uint32_t *slots, uint32_t k, int engine,
+                          uint32_t *counts, int64_t *bins, uint8_t *rgba, int64_t *gram,
+                          int device_outputs, int *fused);
 /* Duration (ms, CUDA events on the ensemble's compute stream) of the most recent
  * launch of each kernel family: 0 = transform (pack, last item), 1 = fused overlap,
- * 2 = Gram (all launches of the call).  Blocks until that launch has finished.     */
+ * 2 = Gram (all launches of the call), 3 = a whole fs_ensemble_recompute call.
+ * Blocks until that launch has finished.                                            */
 #define FS_KERNEL_PACK 0
 #define FS_KERNEL_OVERLAP 1
 #define FS_KERNEL_GRAM 2
+#define FS_KERNEL_RECOMPUTE 3
 int fs_ensemble_kernel_ms(fs_ensemble *ens, int kind, float *ms);
 /* The ensemble's compute stream (cudaStream_t) so callers can order collectives and
  * timing events after its work when device_outputs is used.                      */
@@ -166,6 +177,17 @@ int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *i
 int fs_outlier_scores(const double *sim, uint32_t n, double *scores);
 /* sim[i,j] = inter/union (1.0 when union == 0), diag 1.0, from an int64 Gram.      */
 int fs_similarity_from_gram(const int64_t *gram, uint32_t n, double *sim);
+
+/* ---- measured timings: the reference's modelled costs, on the device -----------
+ * fs_time_transform: mean / min µs (CUDA events, `reps` back-to-back launches) of the
+ * binarize + bit-pack transform of one width x height raster already in HBM (iid
+ * p = 0.5 depths) — replaces transform_time (device.py:384-390) in the sweep of
+ * bench.py:312-339.  engine -1 = current default, 0 = TMA bulk, 1 = direct.
+ * fs_time_h2d: one host->device copy of `bytes` from pinned (or pageable) memory —
+ * replaces transfer_time (device.py:376-382) in the transfer suite (bench.py:193-228). */
+int fs_time_transform(uint32_t width, uint32_t height, int reps, int engine, double *us_mean,
+                      double *us_min);
+int fs_time_h2d(uint64_t bytes, int reps, int pinned, double *us_mean, double *us_min);
 
 /* ---- synthetic input (bench / tests): identical bytes on host and device -------
  * Flood-like prototype+flip generator: mask index i belongs to prototype

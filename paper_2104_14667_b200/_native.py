@@ -20,7 +20,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libfloodstream.so"
 FS_OK, FS_EINVAL, FS_ECUDA, FS_ENOMEM, FS_ENODEV = 0, 1, 2, 3, 4
 VARIANT_CODES = {"1b-initial": 0, "2b-initial": 1, "1b-final": 2, "2b-final": 3}
 GRAM_AUTO, GRAM_POPC, GRAM_TC_I8, GRAM_TC_F4 = 0, 1, 2, 3
-KERNEL_PACK, KERNEL_OVERLAP, KERNEL_GRAM = 0, 1, 2
+KERNEL_PACK, KERNEL_OVERLAP, KERNEL_GRAM, KERNEL_RECOMPUTE = 0, 1, 2, 3
 
 
 class StreamItem(C.Structure):
@@ -73,6 +73,8 @@ _SIGNATURES = {
                             C.c_int],
     "fs_ensemble_running_counts": [_vp, _vp, _vp, _vp, C.c_uint64, C.c_int],
     "fs_ensemble_gram": [_vp, _u32p, C.c_uint32, C.c_int, _vp, C.c_int],
+    "fs_ensemble_recompute": [_vp, _u32p, C.c_uint32, C.c_int, _vp, _vp, _vp, _vp, C.c_int,
+                              C.POINTER(C.c_int)],
     "fs_ensemble_kernel_ms": [_vp, C.c_int, C.POINTER(C.c_float)],
     "fs_ensemble_stream_handle": [_vp, C.POINTER(_vp)],
     "fs_ensemble_sync": [_vp],
@@ -85,6 +87,9 @@ _SIGNATURES = {
     "fs_cluster_complete_linkage": [_f64p, C.c_uint32, _u32p, C.c_double, _i32p],
     "fs_outlier_scores": [_f64p, C.c_uint32, _f64p],
     "fs_similarity_from_gram": [_i64p, C.c_uint32, _f64p],
+    "fs_time_transform": [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.POINTER(C.c_double),
+                          C.POINTER(C.c_double)],
+    "fs_time_h2d": [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "fs_synth_host": [_vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
                       C.c_uint64, C.c_uint32, C.c_double, C.c_int],
 }

@@ -21,7 +21,7 @@ LIB = LIB_DIR / "libfloodstream.so"
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["fs_kernels.cu", "fs_gram_tc.cu", "fs_capi.cu"]
-HEADERS = ["fs_common.cuh", "fs_internal.h"]
+HEADERS = ["fs_common.cuh", "fs_internal.h", "fs_bitslice.cuh"]
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

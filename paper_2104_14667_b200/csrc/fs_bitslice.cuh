@@ -1,0 +1,165 @@
+// fs_bitslice.cuh — device building blocks shared by the fused overlap pass and the
+// fused Gram+overlap kernel: bit-sliced (Harley-Seal) mask counters, the exact composite
+// colour, and the per-tile epilogue (histogram + counts + RGBA) of one warp.
+//
+// Reference semantics: accumulate_into (_kernels_np.py:16-18), overlap_counts
+// (:21-23), composite_fill (:35-47) of /root/reference/pkg/src/floodstream/.
+#pragma once
+#include "fs_internal.h"
+
+namespace fs {
+
+// grey level g = floor(255 (1 - c / max(n, 1)) + 0.5) in FP64 (or from the host LUT)
+__device__ __forceinline__ uint32_t grey_dev(uint64_t c, uint64_t n_inputs, const uint8_t *lut) {
+  if (lut != nullptr) return __ldg(lut + c);
+  double denom = (double)(n_inputs > 0 ? n_inputs : 1);
+  double sat = __ddiv_rn((double)c, denom);
+  double g = floor(__dadd_rn(__dmul_rn(255.0, __dsub_rn(1.0, sat)), 0.5));
+  long long gi = (long long)g;
+  return (uint32_t)(gi & 0xFF);
+}
+// RGBA (g, g, 255, 255) as one little-endian word; 0 when uncovered
+__device__ __forceinline__ uint32_t rgba_word(uint32_t c, uint64_t n_inputs, const uint8_t *lut) {
+  if (c == 0) return 0u;
+  uint32_t g = grey_dev(c, n_inputs, lut);
+  return g | (g << 8) | 0xFFFF0000u;
+}
+
+// carry-save adder: (h, l) = a + b + c
+__device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b,
+                                    uint32_t c) {
+  const uint32_t u = a ^ b;
+  h = (a & b) | (u & c);
+  l = u ^ c;
+}
+
+// Bit-sliced counter of 32 pixels: planes ones/twos/fours/eights plus NH ripple planes
+// of sixteens, so one pass counts up to 16 (2^NH - 1) + 15 masks.
+template <int NH>
+struct HSCounter {
+  uint32_t ones, twos, fours, eights;
+  uint32_t H[NH];
+  __device__ __forceinline__ void reset() {
+    ones = twos = fours = eights = 0;
+#pragma unroll
+    for (int i = 0; i < NH; ++i) H[i] = 0;
+  }
+  __device__ __forceinline__ void add16(const uint32_t (&d)[16]) {
+    uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
+    csa(twosA, ones, ones, d[0], d[1]);
+    csa(twosB, ones, ones, d[2], d[3]);
+    csa(foursA, twos, twos, twosA, twosB);
+    csa(twosA, ones, ones, d[4], d[5]);
+    csa(twosB, ones, ones, d[6], d[7]);
+    csa(foursB, twos, twos, twosA, twosB);
+    csa(eightsA, fours, fours, foursA, foursB);
+    csa(twosA, ones, ones, d[8], d[9]);
+    csa(twosB, ones, ones, d[10], d[11]);
+    csa(foursA, twos, twos, twosA, twosB);
+    csa(twosA, ones, ones, d[12], d[13]);
+    csa(twosB, ones, ones, d[14], d[15]);
+    csa(foursB, twos, twos, twosA, twosB);
+    csa(eightsB, fours, fours, foursA, foursB);
+    csa(sixteens, eights, eights, eightsA, eightsB);
+    uint32_t carry = sixteens;
+#pragma unroll
+    for (int i = 0; i < NH; ++i) {
+      const uint32_t t = H[i] & carry;
+      H[i] ^= carry;
+      carry = t;
+    }
+  }
+  // cnt[j] += wt * count(pixel j)
+  __device__ __forceinline__ void extract(uint32_t (&cnt)[32], uint32_t wt) const {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      uint32_t c = ((ones >> j) & 1u) | (((twos >> j) & 1u) << 1) |
+                   (((fours >> j) & 1u) << 2) | (((eights >> j) & 1u) << 3);
+#pragma unroll
+      for (int i = 0; i < NH; ++i) c |= ((H[i] >> j) & 1u) << (4 + i);
+      cnt[j] += wt * c;
+    }
+  }
+};
+
+__device__ __forceinline__ void st_cs_v4(void *p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+constexpr int kTileTb = 36;  // transpose row stride (words): 16-B aligned, conflict-free v4
+
+// One warp emits one 1024-px tile (tile index `tile`, pixels 1024*tile + 32*w + b):
+// cnt32[b] = count of pixel b of word `lane`.  `tb` is this warp's 32 x kTileTb SMEM
+// scratch.  Histogram: run-length over the lane's 32 consecutive pixels into the SMEM
+// bins (or global bins); padding pixels past a.pixels are counted in bin 0 and must be
+// removed once by the caller.  Counts / RGBA: transposed through `tb` and written with
+// 16-B streaming stores.
+__device__ __forceinline__ void emit_tile(const uint32_t (&cnt32)[32], uint64_t tile, int lane,
+                                          uint32_t *tb, const OverlapArgs &a, uint32_t *sh_hist,
+                                          bool hist_sh, const uint32_t *sh_lut, bool lut_sh) {
+  if (a.bins != nullptr) {
+    uint32_t cur = cnt32[0], run = 1;
+#pragma unroll
+    for (int j = 1; j < 32; ++j) {
+      const uint32_t c = cnt32[j];
+      if (c != cur) {
+        if (hist_sh)
+          atomicAdd(sh_hist + cur, run);
+        else if (cur < a.nbins)
+          atomicAdd(a.bins + cur, (unsigned long long)run);
+        cur = c;
+        run = 0;
+      }
+      ++run;
+    }
+    if (hist_sh)
+      atomicAdd(sh_hist + cur, run);
+    else if (cur < a.nbins)
+      atomicAdd(a.bins + cur, (unsigned long long)run);
+  }
+  if (a.counts == nullptr && a.rgba == nullptr) return;
+  uint32_t *row = tb + lane * kTileTb;
+#pragma unroll
+  for (int v = 0; v < 8; ++v)
+    *reinterpret_cast<uint4 *>(row + 4 * v) =
+        make_uint4(cnt32[4 * v], cnt32[4 * v + 1], cnt32[4 * v + 2], cnt32[4 * v + 3]);
+  __syncwarp();
+  const uint64_t wbase = tile * 32;
+#pragma unroll 2
+  for (int it = 0; it < 8; ++it) {
+    const int w = it * 4 + (lane >> 3), b0 = (lane & 7) * 4;
+    const uint4 c = *reinterpret_cast<const uint4 *>(tb + w * kTileTb + b0);
+    const uint64_t px0 = (wbase + w) * 32 + b0;
+    uint4 r = make_uint4(0, 0, 0, 0);
+    if (a.rgba != nullptr) {
+      if (lut_sh) {
+        r.x = sh_lut[c.x];
+        r.y = sh_lut[c.y];
+        r.z = sh_lut[c.z];
+        r.w = sh_lut[c.w];
+      } else {
+        r.x = rgba_word(c.x, a.n_inputs, a.lut);
+        r.y = rgba_word(c.y, a.n_inputs, a.lut);
+        r.z = rgba_word(c.z, a.n_inputs, a.lut);
+        r.w = rgba_word(c.w, a.n_inputs, a.lut);
+      }
+    }
+    if (a.vec && px0 + 4 <= a.pixels) {
+      if (a.counts) st_cs_v4(a.counts + px0, c);
+      if (a.rgba) st_cs_v4(a.rgba + px0, r);
+    } else {
+      const uint32_t cv[4] = {c.x, c.y, c.z, c.w}, rv[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (px0 + e < a.pixels) {
+          if (a.counts) a.counts[px0 + e] = cv[e];
+          if (a.rgba) a.rgba[px0 + e] = rv[e];
+        }
+    }
+  }
+  __syncwarp();
+}
+
+}  // namespace fs

@@ -409,8 +409,8 @@ struct fs_ensemble {
   uint64_t lut_n = UINT64_MAX;
   cudaStream_t sc = nullptr, sk = nullptr;
   cudaStream_t sk_own = nullptr;  // the ensemble's own compute stream
-  cudaEvent_t kev[3][2] = {};  // per kernel family: start/end
-  bool kev_valid[3] = {false, false, false};
+  cudaEvent_t kev[4][2] = {};  // per kernel family: start/end
+  bool kev_valid[4] = {false, false, false, false};
   std::vector<cudaEvent_t> pool;  // timing events for streaming
   int num_sms = 148;
 };
@@ -476,7 +476,7 @@ int fs_ensemble_create(uint64_t pixels, uint32_t capacity, fs_ensemble **out) {
   CK(cudaStreamCreateWithFlags(&e->sc, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&e->sk_own, cudaStreamNonBlocking));
   e->sk = e->sk_own;
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 4; ++i)
     for (int j = 0; j < 2; ++j) CK(cudaEventCreate(&e->kev[i][j]));
   *out = e.release();
   return FS_OK;
@@ -503,7 +503,7 @@ int fs_ensemble_destroy(fs_ensemble *e) {
     e->lut.release();
     e->gather.release();
     for (auto ev : e->pool) cudaEventDestroy(ev);
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 4; ++i)
       for (int j = 0; j < 2; ++j) cudaEventDestroy(e->kev[i][j]);
     cudaStreamDestroy(e->sc);
     cudaStreamDestroy(e->sk_own);
@@ -561,7 +561,7 @@ int fs_ensemble_sync(fs_ensemble *e) {
 }
 
 int fs_ensemble_kernel_ms(fs_ensemble *e, int kind, float *ms) {
-  if (!e || !ms || kind < 0 || kind > 2) return set_err(FS_EINVAL, "bad argument");
+  if (!e || !ms || kind < 0 || kind > 3) return set_err(FS_EINVAL, "bad argument");
   std::lock_guard<std::mutex> g(e->mu);
   DeviceGuard dg(e->device);
   if (!e->kev_valid[kind]) return set_err(FS_EINVAL, "no launch of that kernel yet");
@@ -688,21 +688,18 @@ int fs_ensemble_synth(fs_ensemble *e, uint32_t first, uint32_t k, uint64_t seed,
   return FS_OK;
 }
 
-int fs_ensemble_overlap(fs_ensemble *e, const uint32_t *slots, uint32_t k, uint64_t cycles,
-                        uint32_t remainder, uint32_t *counts, int64_t *bins, uint8_t *rgba,
-                        int device_outputs) {
-  if (!e) return set_err(FS_EINVAL, "null ensemble");
-  if (k == 0) return set_err(FS_EINVAL, "need at least one surface");
-  if (!slots) return set_err(FS_EINVAL, "null slots");
-  if (remainder > k) return set_err(FS_EINVAL, "remainder exceeds k");
+}  // extern "C"
+
+namespace {
+
+// Output plumbing of the overlap products: device pointers (caller's or the ensemble's
+// scratch), the grey LUT, zeroed bins.  Caller holds the lock and uploaded the slots.
+int prepare_overlap(fs_ensemble *e, const uint32_t *slots, uint32_t k, uint64_t cycles,
+                    uint32_t remainder, uint32_t *counts, int64_t *bins, uint8_t *rgba,
+                    int device_outputs, OverlapArgs &a) {
   const uint64_t n_inputs = cycles * k + remainder;
-  if (n_inputs >= (1ull << 32)) return set_err(FS_EINVAL, "accumulation counts would overflow 32 bits");
-  std::lock_guard<std::mutex> g(e->mu);
-  DeviceGuard dg(e->device);
-  int rc = upload_slots(e, slots, k);
-  if (rc) return rc;
   const uint64_t P = e->pixels, nbins = n_inputs + 1;
-  OverlapArgs a{};
+  a = OverlapArgs{};
   a.packed = e->packed;
   a.capacity = e->capacity;
   a.wpm = e->wpm;
@@ -731,7 +728,7 @@ int fs_ensemble_overlap(fs_ensemble *e, const uint32_t *slots, uint32_t k, uint6
       CK(e->rgba.ensure(P * 4));
       a.rgba = e->rgba.as<uint32_t>();
     }
-    rc = upload_lut(e->lut, e->lut_n, n_inputs, e->sk, &a.lut);
+    int rc = upload_lut(e->lut, e->lut_n, n_inputs, e->sk, &a.lut);
     if (rc) return rc;
   }
   if (bins) {
@@ -743,15 +740,75 @@ int fs_ensemble_overlap(fs_ensemble *e, const uint32_t *slots, uint32_t k, uint6
     }
     CK(cudaMemsetAsync(a.bins, 0, nbins * 8, e->sk));
   }
+  a.vec = ((reinterpret_cast<uintptr_t>(a.counts) | reinterpret_cast<uintptr_t>(a.rgba)) & 15) == 0;
+  return FS_OK;
+}
+
+int overlap_to_host(fs_ensemble *e, const OverlapArgs &a, uint32_t *counts, int64_t *bins,
+                    uint8_t *rgba) {
+  if (counts) CK(cudaMemcpyAsync(counts, a.counts, a.pixels * 4, cudaMemcpyDeviceToHost, e->sk));
+  if (rgba) CK(cudaMemcpyAsync(rgba, a.rgba, a.pixels * 4, cudaMemcpyDeviceToHost, e->sk));
+  if (bins) CK(cudaMemcpyAsync(bins, a.bins, a.nbins * 8, cudaMemcpyDeviceToHost, e->sk));
+  return FS_OK;
+}
+
+int check_engine(int &engine) {
+  if (engine == FS_GRAM_AUTO) engine = g_gram_engine.load();
+  if (engine != FS_GRAM_POPC && engine != FS_GRAM_TC_I8 && engine != FS_GRAM_TC_F4)
+    return set_err(FS_EINVAL, "unknown gram engine");
+  return FS_OK;
+}
+
+// Gram of the uploaded slots into device gd (k x k int64); with `fuse`, the overlap
+// products may be produced by the same kernel (*fused tells).
+int gram_dispatch(fs_ensemble *e, const uint32_t *slots, uint32_t k, int engine,
+                  unsigned long long *gd, const OverlapArgs *fuse, bool *fused) {
+  if (fused) *fused = false;
+  if (engine == FS_GRAM_POPC) {
+    CK(cudaMemsetAsync(gd, 0, (size_t)k * k * 8, e->sk));
+    CK(launch_gram_popc(e->packed, e->capacity, e->wpm, e->slots.as<uint32_t>(), k, gd, e->sk));
+    return FS_OK;
+  }
+  const bool fp4 = engine == FS_GRAM_TC_F4;
+  CK(e->ws.ensure(gram_tc_workspace_bytes(k, e->wpm, e->num_sms, fp4)));
+  void *gws = nullptr;
+  if (contiguous_run(slots, k) < 0) {
+    CK(e->gather.ensure(gram_tc_gather_bytes(k, e->wpm)));
+    gws = e->gather.p;
+  }
+  CK(launch_gram_tc(e->packed, e->capacity, e->wpm, e->slots.as<uint32_t>(), slots, k, gd,
+                    e->ws.p, gws, e->num_sms, fp4, fuse, fused, e->sk));
+  return FS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fs_ensemble_overlap(fs_ensemble *e, const uint32_t *slots, uint32_t k, uint64_t cycles,
+                        uint32_t remainder, uint32_t *counts, int64_t *bins, uint8_t *rgba,
+                        int device_outputs) {
+  if (!e) return set_err(FS_EINVAL, "null ensemble");
+  if (k == 0) return set_err(FS_EINVAL, "need at least one surface");
+  if (!slots) return set_err(FS_EINVAL, "null slots");
+  if (remainder > k) return set_err(FS_EINVAL, "remainder exceeds k");
+  const uint64_t n_inputs = cycles * k + remainder;
+  if (n_inputs >= (1ull << 32)) return set_err(FS_EINVAL, "accumulation counts would overflow 32 bits");
+  std::lock_guard<std::mutex> g(e->mu);
+  DeviceGuard dg(e->device);
+  int rc = upload_slots(e, slots, k);
+  if (rc) return rc;
+  OverlapArgs a;
+  rc = prepare_overlap(e, slots, k, cycles, remainder, counts, bins, rgba, device_outputs, a);
+  if (rc) return rc;
   rc = record_kernel(e, FS_KERNEL_OVERLAP, true);
   if (rc) return rc;
   CK(launch_overlap(a, e->sk));
   rc = record_kernel(e, FS_KERNEL_OVERLAP, false);
   if (rc) return rc;
   if (!device_outputs) {
-    if (counts) CK(cudaMemcpyAsync(counts, a.counts, P * 4, cudaMemcpyDeviceToHost, e->sk));
-    if (rgba) CK(cudaMemcpyAsync(rgba, a.rgba, P * 4, cudaMemcpyDeviceToHost, e->sk));
-    if (bins) CK(cudaMemcpyAsync(bins, a.bins, nbins * 8, cudaMemcpyDeviceToHost, e->sk));
+    rc = overlap_to_host(e, a, counts, bins, rgba);
+    if (rc) return rc;
     CK(cudaStreamSynchronize(e->sk));
   }
   return FS_OK;
@@ -802,13 +859,11 @@ int fs_ensemble_gram(fs_ensemble *e, const uint32_t *slots, uint32_t k, int engi
   if (!e || !gram) return set_err(FS_EINVAL, "null argument");
   if (k == 0) return FS_OK;
   if (!slots) return set_err(FS_EINVAL, "null slots");
-  if (engine == FS_GRAM_AUTO) engine = g_gram_engine.load();
-  if (engine != FS_GRAM_POPC && engine != FS_GRAM_TC_I8 && engine != FS_GRAM_TC_F4)
-    return set_err(FS_EINVAL, "unknown gram engine");
-  const bool fp4 = engine == FS_GRAM_TC_F4;
+  int rc = check_engine(engine);
+  if (rc) return rc;
   std::lock_guard<std::mutex> g(e->mu);
   DeviceGuard dg(e->device);
-  int rc = upload_slots(e, slots, k);
+  rc = upload_slots(e, slots, k);
   if (rc) return rc;
   const size_t gbytes = (size_t)k * k * 8;
   unsigned long long *gd;
@@ -820,23 +875,57 @@ int fs_ensemble_gram(fs_ensemble *e, const uint32_t *slots, uint32_t k, int engi
   }
   rc = record_kernel(e, FS_KERNEL_GRAM, true);
   if (rc) return rc;
-  if (engine == FS_GRAM_POPC) {
-    CK(cudaMemsetAsync(gd, 0, gbytes, e->sk));
-    CK(launch_gram_popc(e->packed, e->capacity, e->wpm, e->slots.as<uint32_t>(), k, gd, e->sk));
-  } else {
-    CK(e->ws.ensure(gram_tc_workspace_bytes(k, e->wpm, e->num_sms, fp4)));
-    void *gws = nullptr;
-    if (contiguous_run(slots, k) < 0) {
-      CK(e->gather.ensure(gram_tc_gather_bytes(k, e->wpm)));
-      gws = e->gather.p;
-    }
-    CK(launch_gram_tc(e->packed, e->capacity, e->wpm, e->slots.as<uint32_t>(), slots, k, gd,
-                      e->ws.p, gws, e->num_sms, fp4, e->sk));
-  }
+  rc = gram_dispatch(e, slots, k, engine, gd, nullptr, nullptr);
+  if (rc) return rc;
   rc = record_kernel(e, FS_KERNEL_GRAM, false);
   if (rc) return rc;
   if (!device_outputs) {
     CK(cudaMemcpyAsync(gram, gd, gbytes, cudaMemcpyDeviceToHost, e->sk));
+    CK(cudaStreamSynchronize(e->sk));
+  }
+  return FS_OK;
+}
+
+int fs_ensemble_recompute(fs_ensemble *e, const uint32_t *slots, uint32_t k, int engine,
+                          uint32_t *counts, int64_t *bins, uint8_t *rgba, int64_t *gram,
+                          int device_outputs, int *fused_out) {
+  if (!e) return set_err(FS_EINVAL, "null ensemble");
+  if (k == 0) return set_err(FS_EINVAL, "need at least one surface");
+  if (!slots) return set_err(FS_EINVAL, "null slots");
+  int rc = check_engine(engine);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(e->mu);
+  DeviceGuard dg(e->device);
+  rc = upload_slots(e, slots, k);
+  if (rc) return rc;
+  OverlapArgs a;
+  rc = prepare_overlap(e, slots, k, 1, 0, counts, bins, rgba, device_outputs, a);
+  if (rc) return rc;
+  const size_t gbytes = (size_t)k * k * 8;
+  unsigned long long *gd = nullptr;
+  if (gram) {
+    if (device_outputs)
+      gd = reinterpret_cast<unsigned long long *>(gram);
+    else {
+      CK(e->gram.ensure(gbytes));
+      gd = e->gram.as<unsigned long long>();
+    }
+  }
+  rc = record_kernel(e, FS_KERNEL_RECOMPUTE, true);
+  if (rc) return rc;
+  bool fused = false;
+  if (gd) {
+    rc = gram_dispatch(e, slots, k, engine, gd, &a, &fused);
+    if (rc) return rc;
+  }
+  if (!fused) CK(launch_overlap(a, e->sk));
+  rc = record_kernel(e, FS_KERNEL_RECOMPUTE, false);
+  if (rc) return rc;
+  if (fused_out) *fused_out = fused ? 1 : 0;
+  if (!device_outputs) {
+    rc = overlap_to_host(e, a, counts, bins, rgba);
+    if (rc) return rc;
+    if (gram) CK(cudaMemcpyAsync(gram, gd, gbytes, cudaMemcpyDeviceToHost, e->sk));
     CK(cudaStreamSynchronize(e->sk));
   }
   return FS_OK;
@@ -1068,6 +1157,84 @@ int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *i
   int32_t p = 0;
   for (uint32_t x : live) pos[x] = p++;
   for (uint32_t i = 0; i < n; ++i) label[i] = pos[owner[i]];
+  return FS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// measured transform / transfer timings (the reference's modelled transform_time and
+// transfer_time, fs/device.py:376-401, and its sweep suites, fs/bench.py:193-339)
+// ---------------------------------------------------------------------------
+int fs_time_transform(uint32_t width, uint32_t height, int reps, int engine, double *us_mean,
+                      double *us_min) {
+  if (!us_mean || !us_min) return set_err(FS_EINVAL, "null out");
+  if (width == 0 || height == 0 || reps < 1) return set_err(FS_EINVAL, "bad sweep cell");
+  if (engine < -1 || engine > 1) return set_err(FS_EINVAL, "unknown pack engine");
+  ThreadCtx *c;
+  int rc = get_ctx(&c);
+  if (rc) return rc;
+  const uint64_t P = (uint64_t)width * height, wpm = words_for_pixels(P);
+  CK(c->a.ensure(P));
+  CK(c->b.ensure(wpm * 4));
+  CK(launch_fill_random(c->a.as<uint8_t>(), P, 0x5EED0000ull + P, c->s));
+  for (int i = 0; i < 2; ++i)  // warm-up
+    CK(launch_pack(c->a.as<uint8_t>(), P, c->b.as<uint32_t>(), 0, 1, wpm, c->s, engine));
+  std::vector<cudaEvent_t> ev((size_t)reps + 1);
+  for (auto &x : ev) CK(cudaEventCreate(&x));
+  CK(cudaEventRecord(ev[0], c->s));
+  for (int i = 0; i < reps; ++i) {
+    CK(launch_pack(c->a.as<uint8_t>(), P, c->b.as<uint32_t>(), 0, 1, wpm, c->s, engine));
+    CK(cudaEventRecord(ev[(size_t)i + 1], c->s));
+  }
+  CK(cudaEventSynchronize(ev[(size_t)reps]));
+  float tot = 0.f, mn = 1e30f;
+  for (int i = 0; i < reps; ++i) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev[(size_t)i], ev[(size_t)i + 1]));
+    tot += ms;
+    mn = std::min(mn, ms);
+  }
+  for (auto &x : ev) cudaEventDestroy(x);
+  *us_mean = (double)tot * 1000.0 / reps;
+  *us_min = (double)mn * 1000.0;
+  return FS_OK;
+}
+
+int fs_time_h2d(uint64_t bytes, int reps, int pinned, double *us_mean, double *us_min) {
+  if (!us_mean || !us_min) return set_err(FS_EINVAL, "null out");
+  if (bytes == 0 || reps < 1) return set_err(FS_EINVAL, "bad transfer size");
+  ThreadCtx *c;
+  int rc = get_ctx(&c);
+  if (rc) return rc;
+  CK(c->a.ensure(bytes));
+  void *h = nullptr;
+  std::vector<uint8_t> pageable;
+  if (pinned) {
+    CK(cudaHostAlloc(&h, bytes, cudaHostAllocPortable));
+  } else {
+    pageable.assign(bytes, 1);
+    h = pageable.data();
+  }
+  std::memset(h, 1, bytes);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  double tot = 0.0, mn = 1e30;
+  for (int i = 0; i < reps + 1; ++i) {
+    CK(cudaEventRecord(e0, c->s));
+    CK(cudaMemcpyAsync(c->a.p, h, bytes, cudaMemcpyHostToDevice, c->s));
+    CK(cudaEventRecord(e1, c->s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (i == 0) continue;  // warm-up
+    tot += ms;
+    mn = std::min(mn, (double)ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (pinned) cudaFreeHost(h);
+  *us_mean = tot * 1000.0 / reps;
+  *us_min = mn * 1000.0;
   return FS_OK;
 }
 

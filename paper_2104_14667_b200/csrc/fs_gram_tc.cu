@@ -30,13 +30,15 @@
 //    range is far below 2^31 pixels.
 #include <cstdio>
 
-#include "fs_internal.h"
+#include "fs_bitslice.cuh"
 
 namespace fs {
 
 namespace tc {
 
 constexpr int kThreads = 192;  // w0: TMEM alloc + MMA; w1..4: expanders + epilogue; w5: TMA
+constexpr int kThreadsFused = 320;  // + w6..9: per-pixel counters (fused overlap pass)
+constexpr int kFuseBins = 288;      // SMEM histogram / RGBA table (k <= 256 -> <= 257 bins)
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kRawDepth = 2;
 
@@ -176,8 +178,14 @@ constexpr uint32_t kSfCol = 448;          // FP4: scale-factor columns [448, 480
 constexpr uint32_t kSfOnes = 0x7F7F7F7Fu; // UE8M0 127 = 2^0 in every byte
 constexpr uint64_t kF4MaxChunkPx = 1ull << 24;  // f32 sums stay exact below this
 
-template <int PANEL, bool DIAG, bool FP4 = false>
+template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false>
 struct Cfg {
+  // raw ring depth.  FUSE: 4 = one slot per counter warp (unit u lives in slot u % 4 and
+  // is counted by warp u % 4), so a counter warp only ever waits on its own slot, in
+  // order, and can never run a full mbarrier phase ahead of it.
+  static constexpr int kDepth = FUSE ? 4 : kRawDepth;
+  static constexpr int kExtraBytes = FUSE ? (4 * 32 * kTileTb * 4 + 2 * kFuseBins * 4) : 0;
+  static constexpr int kBudget = FUSE ? (232448 - 1024 - 256) : kSmemBudget;
   static constexpr int kRowsPerThread = PANEL / 128;  // per region, 128 expander threads
   static constexpr int kRegions = DIAG ? 1 : 2;
   static constexpr int kRawRow = (PANEL == 256 && !DIAG) ? 64 : 128;  // raw bytes/row/unit
@@ -186,21 +194,26 @@ struct Cfg {
   static constexpr int kRawUnitBytes = kRegions * PANEL * kRawRow;
   static constexpr int kRegionBytes = PANEL * 128;
   static constexpr int kStageBytes = kRegionBytes * kRegions;
-  static constexpr int kStagesFit = (kSmemBudget - kRawDepth * kRawUnitBytes) / kStageBytes;
+  static constexpr int kStagesFit =
+      (kBudget - kDepth * kRawUnitBytes - kExtraBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   static constexpr int kHalves = PANEL / 128;
   static constexpr uint32_t kTmemCols = (PANEL == 256 || FP4) ? 512u : 128u;
   static_assert(!FP4 || DIAG, "FP4 path is for diagonal tiles (off-diagonal accumulators fill TMEM)");
-  static constexpr int kSmemBytes =
-      kRawDepth * kRawUnitBytes + kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(!FUSE || DIAG, "the fused overlap pass runs in diagonal tiles");
+  static_assert(!FUSE || kDepth == 4, "counter warp w owns raw slot w");
+  static constexpr int kSmemBytes = kDepth * kRawUnitBytes + kStages * kStageBytes + kExtraBytes +
+                                    1024 /*align*/ + 256 /*barriers*/;
   static_assert(kStages >= 2, "operand ring too shallow");
 };
 
-template <int PANEL, bool DIAG, bool FP4>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int PANEL, bool DIAG, bool FP4, bool FUSE>
+__global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
     k_gram_tc(const __grid_constant__ CUtensorMap tm, uint32_t npanels, uint32_t kchunks,
-              uint64_t units_per_chunk, uint64_t total_units, int32_t *__restrict__ partial) {
-  using C = Cfg<PANEL, DIAG, FP4>;
+              uint64_t units_per_chunk, uint64_t total_units, int32_t *__restrict__ partial,
+              const OverlapArgs ov) {
+  using C = Cfg<PANEL, DIAG, FP4, FUSE>;
+  constexpr int kRawDepth = C::kDepth;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   const uint32_t pad = (1024u - (raw_addr & 1023u)) & 1023u;
@@ -208,8 +221,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t smem_base = raw_addr + pad;
   const uint32_t raw_base = smem_base;                                  // raw ring
   const uint32_t op_base = smem_base + kRawDepth * C::kRawUnitBytes;    // operand stages
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kRawDepth * C::kRawUnitBytes +
-                                                C::kStages * C::kStageBytes);
+  uint8_t *extra = smem + kRawDepth * C::kRawUnitBytes + C::kStages * C::kStageBytes;
+  uint32_t *cnt_tb = reinterpret_cast<uint32_t *>(extra);        // FUSE: 4 x 32 x kTileTb
+  uint32_t *sh_hist = cnt_tb + 4 * 32 * kTileTb;                 // FUSE: kFuseBins
+  uint32_t *sh_lut = sh_hist + kFuseBins;                        // FUSE: kFuseBins
+  uint64_t *full = reinterpret_cast<uint64_t *>(extra + C::kExtraBytes);
   uint64_t *empty = full + C::kStages;
   uint64_t *raw_full = empty + C::kStages;
   uint64_t *raw_empty = raw_full + kRawDepth;
@@ -247,10 +263,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < kRawDepth; ++s) {
       ptx::mbar_init(&raw_full[s], 1);
-      ptx::mbar_init(&raw_empty[s], 128);
+      ptx::mbar_init(&raw_empty[s], FUSE ? 128 + 32 : 128);
     }
     ptx::mbar_init(tmem_full, 1);
     ptx::fence_mbar_init();
+  }
+  const bool lut_sh = FUSE && ov.rgba != nullptr;
+  if (FUSE && tid >= kThreads) {
+    for (int i = tid - kThreads; i < kFuseBins; i += kThreadsFused - kThreads) {
+      sh_hist[i] = 0;
+      sh_lut[i] = lut_sh && (uint32_t)i < ov.nbins ? rgba_word(i, ov.n_inputs, ov.lut) : 0u;
+    }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -334,6 +357,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
+  } else if (FUSE && warp >= 6) {
+    // ===== counters: the fused overlap pass over the same raw tiles =====
+    // warp cw takes units cw, cw+4, ...: lane = word of the 1024-px tile, a bit-sliced
+    // adder over all PANEL mask rows, then the tile epilogue (histogram, counts, RGBA).
+    const int cw = warp - 6;
+    uint32_t off[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      off[j] = ((((uint32_t)lane >> 2) ^ (uint32_t)j) << 4) + ((uint32_t)lane & 3u) * 4u;
+    for (int u = cw; u < nunits; u += 4) {
+      const int ru = u % kRawDepth;
+      ptx::mbar_wait(&raw_full[ru], (uint32_t)((u / kRawDepth) & 1));
+      const uint32_t rb = raw_base + ru * C::kRawUnitBytes;
+      HSCounter<5> hc;
+      hc.reset();
+#pragma unroll 1
+      for (int g16 = 0; g16 < PANEL / 16; ++g16) {
+        uint32_t d[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t addr = rb + (uint32_t)(g16 * 16 + j) * 128u + off[j & 7];
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d[j]) : "r"(addr) : "memory");
+        }
+        hc.add16(d);
+      }
+      __syncwarp();
+      ptx::mbar_arrive(&raw_empty[ru]);
+      uint32_t cnt32[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) cnt32[j] = 0;
+      hc.extract(cnt32, 1u);
+      emit_tile(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
+                ov.bins != nullptr, sh_lut, lut_sh);
+    }
   } else {
     // ===== expanders: raw bits (swizzled) -> 0/1 bytes in SW128 K-major operand =====
     const uint32_t ptid = (uint32_t)(tid - 32);
@@ -403,6 +460,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_before();
   }
   __syncthreads();
+  if (FUSE && tid >= kThreads && ov.bins != nullptr) {
+    for (uint32_t i = tid - kThreads; i < ov.nbins; i += kThreadsFused - kThreads)
+      if (sh_hist[i]) atomicAdd(ov.bins + i, (unsigned long long)sh_hist[i]);
+    if (blockIdx.x == 0 && tid == kThreads) {
+      const uint64_t pad = total_units * 1024 - ov.pixels;  // padding counted in bin 0
+      if (pad) atomicAdd(ov.bins, (unsigned long long)(0ull - pad));
+    }
+  }
   if (warp == 0) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -516,10 +581,10 @@ size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms, bool fp4) 
   return (size_t)(((uint64_t)p.ndiag * p.kc_diag + (uint64_t)p.noff * p.kc_off) * per_tile);
 }
 
-template <int PANEL, bool DIAG, bool FP4 = false>
+template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false>
 static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t *part,
-                              cudaStream_t s) {
-  using C = tc::Cfg<PANEL, DIAG, FP4>;
+                              const OverlapArgs &ov, cudaStream_t s) {
+  using C = tc::Cfg<PANEL, DIAG, FP4, FUSE>;
   const uint32_t ntiles = DIAG ? p.ndiag : p.noff;
   const uint32_t kc = DIAG ? p.kc_diag : p.kc_off;
   const uint64_t upc = DIAG ? p.upc_diag : p.upc_off;
@@ -527,14 +592,15 @@ static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t 
   if (ntiles == 0 || kc == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<PANEL, DIAG, FP4>,
+    cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<PANEL, DIAG, FP4, FUSE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  tc::k_gram_tc<PANEL, DIAG, FP4><<<ntiles * kc, tc::kThreads, C::kSmemBytes, s>>>(
-      tm, p.npanels, kc, upc, units, part);
+  tc::k_gram_tc<PANEL, DIAG, FP4, FUSE>
+      <<<ntiles * kc, FUSE ? tc::kThreadsFused : tc::kThreads, C::kSmemBytes, s>>>(
+          tm, p.npanels, kc, upc, units, part, ov);
   return cudaGetLastError();
 }
 
@@ -543,7 +609,9 @@ size_t gram_tc_gather_bytes(uint32_t k, uint64_t wpm) { return (size_t)k * wpm *
 cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t wpm,
                            const uint32_t *slots, const uint32_t *host_slots, uint32_t k,
                            unsigned long long *gram, void *workspace, void *gather_ws,
-                           int num_sms, bool fp4, cudaStream_t s) {
+                           int num_sms, bool fp4, const OverlapArgs *fuse, bool *fused,
+                           cudaStream_t s) {
+  if (fused) *fused = false;
   if (k == 0) return cudaSuccess;
   tc::Plan p = tc::make_plan(k, wpm, num_sms, fp4);
   const uint64_t ntiles = wpm / 32;
@@ -576,17 +644,30 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
   if ((e = encode_packed_map(&tm_off, src, src_cap, row0, k, ntiles, raw_off, p.panel, 1,
                              raw_off == 16 ? 64 : 128)) != cudaSuccess)
     return e;
+  const OverlapArgs none{};
+  // one panel holds every mask: its diagonal CTAs see all masks of a pixel range and
+  // also produce the overlap products (counts / histogram / RGBA) from the same tiles
+  const bool fuse_now = fuse != nullptr && p.npanels == 1;
   if (p.panel == 128) {
-    e = fp4 ? launch_one<128, true, true>(tm_diag, p, part_diag, s)
-            : launch_one<128, true>(tm_diag, p, part_diag, s);
+    if (fuse_now)
+      e = fp4 ? launch_one<128, true, true, true>(tm_diag, p, part_diag, *fuse, s)
+              : launch_one<128, true, false, true>(tm_diag, p, part_diag, *fuse, s);
+    else
+      e = fp4 ? launch_one<128, true, true>(tm_diag, p, part_diag, none, s)
+              : launch_one<128, true>(tm_diag, p, part_diag, none, s);
     if (e != cudaSuccess) return e;
-    if ((e = launch_one<128, false>(tm_off, p, part_off, s)) != cudaSuccess) return e;
+    if ((e = launch_one<128, false>(tm_off, p, part_off, none, s)) != cudaSuccess) return e;
   } else {
-    e = fp4 ? launch_one<256, true, true>(tm_diag, p, part_diag, s)
-            : launch_one<256, true>(tm_diag, p, part_diag, s);
+    if (fuse_now)
+      e = fp4 ? launch_one<256, true, true, true>(tm_diag, p, part_diag, *fuse, s)
+              : launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s);
+    else
+      e = fp4 ? launch_one<256, true, true>(tm_diag, p, part_diag, none, s)
+              : launch_one<256, true>(tm_diag, p, part_diag, none, s);
     if (e != cudaSuccess) return e;
-    if ((e = launch_one<256, false>(tm_off, p, part_off, s)) != cudaSuccess) return e;
+    if ((e = launch_one<256, false>(tm_off, p, part_off, none, s)) != cudaSuccess) return e;
   }
+  if (fused) *fused = fuse_now;
   const uint64_t total = (uint64_t)(p.ndiag + p.noff) * per_tile;
   uint64_t grid = (total + 255) / 256;
   if (grid > (uint64_t)num_sms * 8) grid = (uint64_t)num_sms * 8;

@@ -30,6 +30,8 @@ int64_t contiguous_run(const uint32_t *host_slots, uint32_t k);
 cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *packed, uint64_t slot,
                         uint64_t capacity, uint64_t wpm, cudaStream_t s, int engine);
 void set_pack_engine(int engine);
+// iid p = 0.5 depth bytes (transform sweep inputs)
+cudaError_t launch_fill_random(uint8_t *dst, uint64_t n, uint64_t seed, cudaStream_t s);
 int get_pack_engine();
 
 // ---- reference primitive protocol kernels (flat device arrays) ----------------
@@ -76,7 +78,11 @@ size_t gram_tc_gather_bytes(uint32_t k, uint64_t wpm);
 cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t wpm,
                            const uint32_t *slots, const uint32_t *host_slots, uint32_t k,
                            unsigned long long *gram, void *workspace, void *gather_ws,
-                           int num_sms, bool fp4, cudaStream_t s);
+                           int num_sms, bool fp4, const OverlapArgs *fuse, bool *fused,
+                           cudaStream_t s);
+// fuse != nullptr: when all k masks fit one panel (k <= 256) the diagonal CTAs also
+// run the overlap pass (counts / histogram / RGBA of `*fuse`, weights 1) and *fused is
+// set; bins must be zeroed by the caller.  Otherwise nothing of *fuse is written.
 // gram (k x k, upper tiles filled) -> symmetric
 cudaError_t launch_gram_mirror(unsigned long long *gram, uint32_t k, uint32_t tile,
                                cudaStream_t s);

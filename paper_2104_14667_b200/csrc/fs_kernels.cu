@@ -16,7 +16,7 @@
 
 #include <cudaTypedefs.h>
 
-#include "fs_internal.h"
+#include "fs_bitslice.cuh"
 
 namespace fs {
 
@@ -45,21 +45,6 @@ __device__ __forceinline__ uint32_t nz_nibble(uint32_t x) {
 __device__ __forceinline__ uint32_t nz_bits16(uint4 v) {
   return nz_nibble(v.x) | (nz_nibble(v.y) << 4) | (nz_nibble(v.z) << 8) |
          (nz_nibble(v.w) << 12);
-}
-
-__device__ __forceinline__ uint32_t grey_dev(uint64_t c, uint64_t n_inputs, const uint8_t *lut) {
-  if (lut != nullptr) return __ldg(lut + c);
-  // FP64, no contraction: sat = c / max(n,1); g = floor(255*(1-sat) + 0.5)
-  double denom = (double)(n_inputs > 0 ? n_inputs : 1);
-  double sat = __ddiv_rn((double)c, denom);
-  double g = floor(__dadd_rn(__dmul_rn(255.0, __dsub_rn(1.0, sat)), 0.5));
-  long long gi = (long long)g;
-  return (uint32_t)(gi & 0xFF);
-}
-__device__ __forceinline__ uint32_t rgba_word(uint32_t c, uint64_t n_inputs, const uint8_t *lut) {
-  if (c == 0) return 0u;
-  uint32_t g = grey_dev(c, n_inputs, lut);
-  return g | (g << 8) | 0xFFFF0000u;  // bytes (g, g, 255, 255), little endian
 }
 
 // ---------------------------------------------------------------------------
@@ -366,71 +351,10 @@ constexpr int kOvThreads = 32 * kOvTiles;
 constexpr int kOvGroup = 16;
 constexpr int kOvStages = 4;
 constexpr int kOvStageWords = kOvTiles * kOvGroup * 32;  // 8 KB
-constexpr int kOvTb = 36;                                 // transpose row stride (words)
 
 static size_t ov_smem_bytes(uint32_t sbins) {
-  return (size_t)kOvStages * kOvStageWords * 4 + (size_t)kOvTiles * 32 * kOvTb * 4 +
+  return (size_t)kOvStages * kOvStageWords * 4 + (size_t)kOvTiles * 32 * kTileTb * 4 +
          2 * kOvStages * 8 + 2 * (size_t)sbins * 4;
-}
-
-__device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b,
-                                    uint32_t c) {
-  const uint32_t u = a ^ b;
-  h = (a & b) | (u & c);
-  l = u ^ c;
-}
-
-template <int NH>
-struct HSCounter {
-  uint32_t ones, twos, fours, eights;
-  uint32_t H[NH];
-  __device__ __forceinline__ void reset() {
-    ones = twos = fours = eights = 0;
-#pragma unroll
-    for (int i = 0; i < NH; ++i) H[i] = 0;
-  }
-  __device__ __forceinline__ void add16(const uint32_t (&d)[16]) {
-    uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
-    csa(twosA, ones, ones, d[0], d[1]);
-    csa(twosB, ones, ones, d[2], d[3]);
-    csa(foursA, twos, twos, twosA, twosB);
-    csa(twosA, ones, ones, d[4], d[5]);
-    csa(twosB, ones, ones, d[6], d[7]);
-    csa(foursB, twos, twos, twosA, twosB);
-    csa(eightsA, fours, fours, foursA, foursB);
-    csa(twosA, ones, ones, d[8], d[9]);
-    csa(twosB, ones, ones, d[10], d[11]);
-    csa(foursA, twos, twos, twosA, twosB);
-    csa(twosA, ones, ones, d[12], d[13]);
-    csa(twosB, ones, ones, d[14], d[15]);
-    csa(foursB, twos, twos, twosA, twosB);
-    csa(eightsB, fours, fours, foursA, foursB);
-    csa(sixteens, eights, eights, eightsA, eightsB);
-    uint32_t carry = sixteens;
-#pragma unroll
-    for (int i = 0; i < NH; ++i) {
-      const uint32_t t = H[i] & carry;
-      H[i] ^= carry;
-      carry = t;
-    }
-  }
-  // cnt[j] += wt * count(pixel j)
-  __device__ __forceinline__ void extract(uint32_t (&cnt)[32], uint32_t wt) const {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      uint32_t c = ((ones >> j) & 1u) | (((twos >> j) & 1u) << 1) |
-                   (((fours >> j) & 1u) << 2) | (((eights >> j) & 1u) << 3);
-#pragma unroll
-      for (int i = 0; i < NH; ++i) c |= ((H[i] >> j) & 1u) << (4 + i);
-      cnt[j] += wt * c;
-    }
-  }
-};
-
-__device__ __forceinline__ void st_cs_v4(void *p, uint4 v) {
-  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
-               "r"(v.z), "r"(v.w)
-               : "memory");
 }
 
 template <bool GATHER, int NH>
@@ -440,7 +364,7 @@ __global__ void __launch_bounds__(kOvThreads)
   extern __shared__ __align__(128) uint8_t sm[];
   uint32_t *stage = reinterpret_cast<uint32_t *>(sm);
   uint32_t *tb = stage + kOvStages * kOvStageWords;
-  uint64_t *full = reinterpret_cast<uint64_t *>(tb + kOvTiles * 32 * kOvTb);
+  uint64_t *full = reinterpret_cast<uint64_t *>(tb + kOvTiles * 32 * kTileTb);
   uint64_t *empty = full + kOvStages;
   uint32_t *sh_hist = reinterpret_cast<uint32_t *>(empty + kOvStages);
   uint32_t *sh_lut = sh_hist + sbins;
@@ -517,7 +441,6 @@ __global__ void __launch_bounds__(kOvThreads)
   uint32_t g = 0;
   int s = 0;
   uint32_t phase = 0;
-  const bool vec = a.vec != 0;
 
   for (uint64_t i = 0; i < nitems; ++i) {
     uint32_t off, cnt;
@@ -553,68 +476,8 @@ __global__ void __launch_bounds__(kOvThreads)
     }
     if (g == GP - 1) {
       const uint64_t tile = (blockIdx.x + q * gridDim.x) * kOvTiles + wi;
-      if (tile < ntiles) {
-        if (do_hist) {
-          // run-length over this word's 32 consecutive pixels
-          uint32_t cur = cnt32[0], run = 1;
-#pragma unroll
-          for (int j = 1; j < 32; ++j) {
-            const uint32_t c = cnt32[j];
-            if (c != cur) {
-              if (hist_sh)
-                atomicAdd(sh_hist + cur, run);
-              else if (cur < a.nbins)
-                atomicAdd(a.bins + cur, (unsigned long long)run);
-              cur = c;
-              run = 0;
-            }
-            ++run;
-          }
-          if (hist_sh)
-            atomicAdd(sh_hist + cur, run);
-          else if (cur < a.nbins)
-            atomicAdd(a.bins + cur, (unsigned long long)run);
-        }
-        if (a.counts != nullptr || a.rgba != nullptr) {
-          uint32_t *row = tb + (wi * 32 + lane) * kOvTb;
-#pragma unroll
-          for (int v = 0; v < 8; ++v)
-            *reinterpret_cast<uint4 *>(row + 4 * v) =
-                make_uint4(cnt32[4 * v], cnt32[4 * v + 1], cnt32[4 * v + 2], cnt32[4 * v + 3]);
-          __syncwarp();
-          const uint64_t wbase = tile * 32;
-#pragma unroll 2
-          for (int it = 0; it < 8; ++it) {
-            const int w = it * 4 + (lane >> 3), b0 = (lane & 7) * 4;
-            const uint4 c = *reinterpret_cast<const uint4 *>(tb + (wi * 32 + w) * kOvTb + b0);
-            const uint64_t px0 = (wbase + w) * 32 + b0;
-            uint4 r = make_uint4(0, 0, 0, 0);
-            if (a.rgba != nullptr) {
-              if (lut_sh) {
-                r.x = sh_lut[c.x]; r.y = sh_lut[c.y]; r.z = sh_lut[c.z]; r.w = sh_lut[c.w];
-              } else {
-                r.x = rgba_word(c.x, a.n_inputs, a.lut);
-                r.y = rgba_word(c.y, a.n_inputs, a.lut);
-                r.z = rgba_word(c.z, a.n_inputs, a.lut);
-                r.w = rgba_word(c.w, a.n_inputs, a.lut);
-              }
-            }
-            if (vec && px0 + 4 <= a.pixels) {
-              if (a.counts) st_cs_v4(a.counts + px0, c);
-              if (a.rgba) st_cs_v4(a.rgba + px0, r);
-            } else {
-              const uint32_t cv[4] = {c.x, c.y, c.z, c.w}, rv[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (px0 + e < a.pixels) {
-                  if (a.counts) a.counts[px0 + e] = cv[e];
-                  if (a.rgba) a.rgba[px0 + e] = rv[e];
-                }
-            }
-          }
-          __syncwarp();
-        }
-      }
+      if (tile < ntiles)
+        emit_tile(cnt32, tile, lane, tb + wi * 32 * kTileTb, a, sh_hist, hist_sh, sh_lut, lut_sh);
 #pragma unroll
       for (int j = 0; j < 32; ++j) cnt32[j] = 0;
     }
@@ -855,6 +718,34 @@ cudaError_t launch_synth_packed(uint32_t *dst, uint64_t slot, uint64_t cap, uint
   const uint64_t gcap = (uint64_t)num_sms() * 16;
   if (grid > gcap) grid = gcap;
   k_synth_packed<<<(unsigned)grid, 256, 0, s>>>(dst, slot, cap, wpm, sp, mask, row0, pixels);
+  return cudaGetLastError();
+}
+
+// iid test rasters for the transform sweep: byte = depth 1..255 with p = 0.5, else 0
+__global__ void k_fill_random(uint8_t *__restrict__ dst, uint64_t n, uint64_t seed) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q * 8 < n; q += stride) {
+    const uint64_t h = mix64(seed ^ (q * 0x9E3779B97F4A7C15ull));
+    uint64_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint64_t byte = (h >> (8 * b)) & 0xFF;
+      v |= ((byte & 1) ? (byte | 1) : 0ull) << (8 * b);
+    }
+    if (q * 8 + 8 <= n) {
+      reinterpret_cast<uint64_t *>(dst)[q] = v;
+    } else {
+      for (uint64_t b = 0; q * 8 + b < n; ++b) dst[q * 8 + b] = (uint8_t)(v >> (8 * b));
+    }
+  }
+}
+
+cudaError_t launch_fill_random(uint8_t *dst, uint64_t n, uint64_t seed, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint64_t grid = (n / 8 + 255) / 256 + 1;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
+  if (grid > cap) grid = cap;
+  k_fill_random<<<(unsigned)grid, 256, 0, s>>>(dst, n, seed);
   return cudaGetLastError();
 }
 

@@ -98,6 +98,9 @@ class ShardedEnsemble:
         self._bufs: dict = {}
 
     def close(self) -> None:
+        if getattr(self, "_pool", None) is not None:
+            self._pool.shutdown(wait=True)
+            self._pool = None
         self.ens.close()
 
     def _make_buffers(self, k: int, n_inputs: int, maps: bool):
@@ -114,6 +117,7 @@ class ShardedEnsemble:
         if maps:
             b["h_counts"] = torch.empty(px, dtype=torch.int32).pin_memory()
             b["h_rgba"] = torch.empty(px * 4, dtype=torch.uint8).pin_memory()
+            b["event_maps"] = torch.cuda.Event()
         return b
 
     def _enqueue(self, sl: np.ndarray, b, *, engine: str, cycles: int = 1, remainder: int = 0,
@@ -124,68 +128,122 @@ class ShardedEnsemble:
         import torch
 
         part = b["part"]
-        self.ens.overlap(sl, cycles=cycles, remainder=remainder,
-                         out_counts=b["counts"].data_ptr(), out_rgba=b["rgba"].data_ptr(),
-                         out_bins=part.data_ptr(), device_outputs=True)
-        self.ens.gram(sl, engine=engine, out=part.data_ptr() + b["nb"] * 8, device_outputs=True)
+        if cycles == 1 and remainder == 0:
+            # one call: fused overlap + Gram when the engine and k allow it
+            self.ens.products(sl, engine=engine, out_counts=b["counts"].data_ptr(),
+                              out_rgba=b["rgba"].data_ptr(), out_bins=part.data_ptr(),
+                              out_gram=part.data_ptr() + b["nb"] * 8, device_outputs=True)
+        else:
+            self.ens.overlap(sl, cycles=cycles, remainder=remainder,
+                             out_counts=b["counts"].data_ptr(), out_rgba=b["rgba"].data_ptr(),
+                             out_bins=part.data_ptr(), device_outputs=True)
+            self.ens.gram(sl, engine=engine, out=part.data_ptr() + b["nb"] * 8,
+                          device_outputs=True)
+        if maps_to_host:
+            # the maps' D2H (8 B/px) runs on a side stream: PCIe is full duplex, so it
+            # overlaps the next frame's H2D upload instead of delaying it
+            if getattr(self, "d2h_stream", None) is None:
+                self.d2h_stream = torch.cuda.Stream(device=self.device)
+            ready = torch.cuda.Event()
+            ready.record(self.stream)
+            self.d2h_stream.wait_event(ready)
+            with torch.cuda.stream(self.d2h_stream):
+                b["h_counts"].copy_(b["counts"], non_blocking=True)
+                b["h_rgba"].copy_(b["rgba"], non_blocking=True)
+                b["event_maps"].record(self.d2h_stream)
         with torch.cuda.stream(self.stream):
             allreduce_partials(part, self.group)
             b["h_part"].copy_(part, non_blocking=True)
-            if maps_to_host:
-                b["h_counts"].copy_(b["counts"], non_blocking=True)
-                b["h_rgba"].copy_(b["rgba"], non_blocking=True)
             b["event"].record(self.stream)
 
-    def _finish(self, b, ids, tau: float, analytics: bool, maps_to_host: bool):
+    def _finish(self, b, ids, tau: float, analytics: bool, maps_to_host: bool, free=None):
+        """Wait for a frame's D2H, copy out its histogram and Gram, run the host
+        analytics; then hand the buffer slot back (``free``).  Runs on a pool thread:
+        the C analytics release the GIL, so frames' host work overlaps each other and
+        the main thread's enqueueing."""
         from .analytics import cluster_from_similarity, outliers_from_similarity, similarity_from_gram
 
-        b["event"].synchronize()
-        part = b["h_part"].numpy()
-        k = b["k"]
-        out = {"bins": part[: b["nb"]].copy(), "gram": part[b["nb"]:].reshape(k, k).copy()}
-        if maps_to_host:
-            # views of the pinned frame buffers: valid until this buffer's next frame
-            # (two frames later) is enqueued — copy them to keep them longer
-            out["counts"] = b["h_counts"].numpy().view(np.uint32).reshape(self.rows, self.width)
-            out["rgba"] = b["h_rgba"].numpy().reshape(self.rows, self.width, 4)
-        if analytics:
-            sim = similarity_from_gram(out["gram"])
-            out["similarity"] = sim
-            out["outliers"] = outliers_from_similarity(sim, ids) if len(ids) >= 2 else None
-            out["clusters"] = cluster_from_similarity(sim, ids, tau)
-        return out
+        try:
+            b["event"].synchronize()
+            part = b["h_part"].numpy()
+            k = b["k"]
+            out = {"bins": part[: b["nb"]].copy(), "gram": part[b["nb"]:].reshape(k, k).copy()}
+            if maps_to_host:
+                b["event_maps"].synchronize()
+                # views of the pinned slot: valid until the slot is reused (``depth``
+                # frames later) — copy them to keep them longer
+                out["counts"] = b["h_counts"].numpy().view(np.uint32).reshape(self.rows, self.width)
+                out["rgba"] = b["h_rgba"].numpy().reshape(self.rows, self.width, 4)
+            else:
+                if free is not None:
+                    free.set()
+                    free = None
+            if analytics:
+                sim = similarity_from_gram(out["gram"])
+                out["similarity"] = sim
+                out["outliers"] = outliers_from_similarity(sim, ids) if len(ids) >= 2 else None
+                out["clusters"] = cluster_from_similarity(sim, ids, tau)
+            return out
+        finally:
+            if free is not None:
+                free.set()
+
+    def _executor(self, workers: int):
+        from concurrent.futures import ThreadPoolExecutor
+
+        if getattr(self, "_pool", None) is None or self._pool_workers != workers:
+            if getattr(self, "_pool", None) is not None:
+                self._pool.shutdown(wait=True)
+            self._pool = ThreadPoolExecutor(max_workers=workers, thread_name_prefix="fs-frames")
+            self._pool_workers = workers
+        return self._pool
 
     def run_frames(self, slots, n_frames: int, *, tau: float = 0.8, engine: str = "auto",
                    ids=None, maps_to_host: bool = False, analytics_ranks: str = "all",
-                   before_frame=None, keep: bool = True):
-        """``n_frames`` full recomputes of the working set, double-buffered: frame f+1's
-        device work (overlap, Gram, all-reduce, D2H) is enqueued before frame f's host
-        analytics (Jaccard, outliers, clusters) run, so the two overlap — the
-        interactive-recompute loop of service.py:143-175 at GPU rate.
-        ``before_frame(f)`` runs first in each frame (e.g. streaming new rasters in).
-        Returns the per-frame results (only the last one unless ``keep``)."""
+                   before_frame=None, keep: bool = True, depth: int = 3):
+        """``n_frames`` full recomputes of the working set, pipelined over a ring of
+        ``depth`` frame buffers: the main thread keeps enqueueing device work
+        (overlap + Gram, all-reduce, D2H) while pool threads wait for earlier frames and
+        run their host analytics (Jaccard, outliers, clusters) — the interactive
+        recompute loop of service.py:143-175 at GPU rate.  ``before_frame(f)`` runs first
+        in each frame (e.g. streaming new rasters in).  Results come back in frame
+        order (only the last one unless ``keep``)."""
+        import threading
+        from collections import deque
+
         sl = np.ascontiguousarray(np.asarray(list(slots), dtype=np.uint32))
         k = int(sl.size)
         ids = list(ids) if ids is not None else [f"s{i:04d}" for i in sl.tolist()]
-        key = (k, maps_to_host)
+        depth = max(2, int(depth))
+        key = (k, maps_to_host, depth)
         if self._bufs.get("key") != key:
-            self._bufs = {"key": key, "b": [self._make_buffers(k, k, maps_to_host) for _ in range(2)]}
-        bufs = self._bufs["b"]
+            self._bufs = {"key": key,
+                          "b": [self._make_buffers(k, k, maps_to_host) for _ in range(depth)],
+                          "free": [threading.Event() for _ in range(depth)]}
+            for e in self._bufs["free"]:
+                e.set()
+        bufs, free = self._bufs["b"], self._bufs["free"]
+        pool = self._executor(depth)
         # "all": every rank runs the host analytics; "root": rank 0 only; "none": skip
         analytics = analytics_ranks == "all" or (analytics_ranks == "root" and self.rank == 0)
-        results, pending = [], None
+        results, futs = [], deque()
         for f in range(n_frames):
             if before_frame is not None:
                 before_frame(f)
-            b = bufs[f % 2]
-            self._enqueue(sl, b, engine=engine, maps_to_host=maps_to_host)
-            if pending is not None:
-                r = self._finish(pending, ids, tau, analytics, maps_to_host)
+            i = f % depth
+            free[i].wait()
+            free[i].clear()
+            self._enqueue(sl, bufs[i], engine=engine, maps_to_host=maps_to_host)
+            futs.append(pool.submit(self._finish, bufs[i], ids, tau, analytics, maps_to_host,
+                                    free[i]))
+            while futs and futs[0].done():
+                r = futs.popleft().result()
                 if keep:
                     results.append(r)
-            pending = b
-        if pending is not None:
-            results.append(self._finish(pending, ids, tau, analytics, maps_to_host))
+        while futs:
+            r = futs.popleft().result()
+            if keep or not futs:
+                results.append(r)
         return results if keep else results[-1:]
 
     def recompute(self, slots, *, tau: float = 0.8, engine: str = "auto", ids=None):

@@ -131,7 +131,8 @@ class DeviceEnsemble:
         N.call("fs_ensemble_sync", self._h)
 
     def kernel_ms(self, kind: str) -> float:
-        code = {"pack": N.KERNEL_PACK, "overlap": N.KERNEL_OVERLAP, "gram": N.KERNEL_GRAM}[kind]
+        code = {"pack": N.KERNEL_PACK, "overlap": N.KERNEL_OVERLAP, "gram": N.KERNEL_GRAM,
+                "recompute": N.KERNEL_RECOMPUTE}[kind]
         ms = C.c_float()
         N.call("fs_ensemble_kernel_ms", self._h, code, C.byref(ms))
         return float(ms.value)
@@ -243,6 +244,34 @@ class DeviceEnsemble:
                N.ptr(g), 0)
         return g
 
+    def products(self, slots=None, *, engine: str = "auto", counts=True, bins=True, rgba=True,
+                 gram=True, out_counts=None, out_bins=None, out_rgba=None, out_gram=None,
+                 device_outputs: bool = False):
+        """Counts, histogram, composite and Gram of ``slots`` in ONE call
+        (fs_ensemble_recompute): with a tensor-core engine and k <= 256 the overlap
+        products come out of the Gram kernel itself (one read of the packed masks).
+        Returns (counts, bins, rgba, gram, fused)."""
+        sl = self._slots(slots)
+        k = int(sl.size)
+        fused = C.c_int(0)
+        if device_outputs:
+            ptrs = [int(p) if (want and p is not None) else None
+                    for want, p in ((counts, out_counts), (bins, out_bins), (rgba, out_rgba),
+                                    (gram, out_gram))]
+            N.call("fs_ensemble_recompute", self._h, sl.ctypes.data_as(N._u32p), k,
+                   _GRAM_ENGINES[engine], *ptrs, 1, C.byref(fused))
+            return out_counts, out_bins, out_rgba, out_gram, bool(fused.value)
+        c = (out_counts if out_counts is not None else
+             np.empty((self.rows, self.width), dtype=np.uint32)) if counts else None
+        b = (out_bins if out_bins is not None else np.empty(k + 1, dtype=np.int64)) if bins else None
+        r = (out_rgba if out_rgba is not None else
+             np.empty((self.rows, self.width, 4), dtype=np.uint8)) if rgba else None
+        g = (out_gram if out_gram is not None else np.empty((k, k), dtype=np.int64)) if gram else None
+        N.call("fs_ensemble_recompute", self._h, sl.ctypes.data_as(N._u32p), k,
+               _GRAM_ENGINES[engine], *[None if x is None else N.ptr(x) for x in (c, b, r, g)], 0,
+               C.byref(fused))
+        return c, b, r, g, bool(fused.value)
+
     def recompute(self, slots=None, *, tau: float = 0.8, engine: str = "auto",
                   overlap: bool = True, pairwise: bool = True) -> Snapshot:
         """Full recompute of the working set: grid, histogram, composite, Gram,
@@ -250,13 +279,17 @@ class DeviceEnsemble:
         sl = self._slots(slots)
         ids = [self.ids[i] if self.ids[i] is not None else f"slot{i}" for i in sl.tolist()]
         grid = hist = comp = gram = sim = outl = clus = None
-        if overlap:
+        if overlap and pairwise:
+            c, b, r, gram, _ = self.products(sl, engine=engine)
+        elif overlap:
             c, b, r = self.overlap(sl)
+        elif pairwise:
+            gram = self.gram(sl, engine=engine)
+        if overlap:
             grid = AccumulationGrid._from_device(self.width, self.rows, int(sl.size), c)
             hist = OverlapHistogram(bins=[int(x) for x in b])
             comp = CompositeImage(width=self.width, height=self.rows, pixels=r)
         if pairwise:
-            gram = self.gram(sl, engine=engine)
             sim = similarity_from_gram(gram)
             if len(ids) >= 2:
                 outl = outliers_from_similarity(sim, ids)

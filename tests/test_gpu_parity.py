@@ -326,3 +326,83 @@ def test_gram_f4_chunk_cap_large_k_range():
         ref = ens.gram(engine="popc")
     assert np.array_equal(got, ref)
     assert got[0, 0] == w * h
+
+
+# ---- fused recompute: overlap products out of the Gram kernel -------------------------
+
+@pytest.mark.parametrize("engine", ["tc-f4", "tc", "popc"])
+@pytest.mark.parametrize("k,h,w", [(1, 5, 7), (3, 33, 31), (16, 64, 64), (100, 40, 70),
+                                   (128, 32, 33), (129, 17, 65), (256, 24, 40),
+                                   (257, 16, 33), (300, 9, 130), (64, 1500, 1100),
+                                   (200, 700, 2000), (256, 613, 1999)])
+def test_products_match_oracle(engine, k, h, w):
+    rng = np.random.default_rng(7 * k + h)
+    cells = [(rng.random((h, w)) < rng.uniform(0.05, 0.95)).astype(np.uint8) *
+             rng.integers(1, 256, (h, w)).astype(np.uint8) for _ in range(k)]
+    want = O.accumulate(cells, w, h)
+    with DeviceEnsemble(w, h, k + 3) as ens:
+        ens.upload(cells, first=2)
+        slots = list(range(2, k + 2))
+        c, b, r, g, fused = ens.products(slots, engine=engine)
+        perm = [2 + int(x) for x in rng.permutation(k)]
+        c2, b2, r2, g2, fused2 = ens.products(perm, engine=engine)  # gathered slots
+    assert fused == (engine != "popc" and k <= 256)
+    assert np.array_equal(c, want)
+    assert b.tolist() == O.overlap_counts(want.reshape(-1), k).tolist()
+    assert np.array_equal(r, O.composite(want, k))
+    gw = O.gram(cells)
+    assert np.array_equal(g, gw)
+    assert np.array_equal(c2, want) and np.array_equal(r2, r) and np.array_equal(b2, b)
+    p = np.asarray(perm) - 2
+    assert np.array_equal(g2, gw[np.ix_(p, p)])
+
+
+def test_products_c1_goldens(golden):
+    """The reference bench inputs through the fused path: every C1 golden."""
+    cells = c1_cells()
+    rec = golden["c1"]
+    with DeviceEnsemble(1024, 1024, 16) as ens:
+        ens.upload(cells)
+        c, b, r, g, fused = ens.products(engine="tc-f4")
+    assert fused
+    assert O.grid_digest(1024, 1024, 16, c) == rec["digest"]
+    assert b.tolist() == rec["bins"]
+    assert sha(r) == rec["composite_sha"]
+    assert sha(g) == rec["gram_sha"]
+
+
+def test_products_c2_scale_fused_equals_unfused():
+    """Config 2 (256 x 8192^2) on the device: the fused kernel's maps, histogram and
+    Gram equal the separate overlap kernel + popc Gram, bit for bit."""
+    w = h = 8192
+    k = 256
+    with DeviceEnsemble(w, h, k) as ens:
+        ens.synth(0, k, seed=2104, members=16, eps=0.02)
+        c, b, r, g, fused = ens.products(engine="tc-f4")
+        c0, b0, r0 = ens.overlap()
+        g0 = ens.gram(engine="popc")
+    assert fused
+    assert np.array_equal(b, b0)
+    assert np.array_equal(g, g0)
+    assert np.array_equal(c, c0)
+    assert np.array_equal(r, r0)
+
+
+# ---- measured sweep suites (config 5) -------------------------------------------------
+
+def test_transform_sweep_and_transfer_suites():
+    from paper_2104_14667_b200.sweep import (RateMap, SweepSpec, render_rate_map,
+                                             run_backend_comparison, run_transfer_baseline,
+                                             run_transform_sweep)
+
+    spec = SweepSpec(64, 500, 1100)
+    rm = run_transform_sweep(spec, reps=2)
+    assert rm.rates.shape == (3, 3) and (rm.rates > 0).all()
+    assert RateMap.from_json(rm.to_json()).rates.tolist() == rm.rates.tolist()
+    assert rm.to_csv().splitlines()[0] == "width,height,rate_gbps"
+    assert render_rate_map(rm).shape == (3, 3, 4)
+    rep = run_transfer_baseline(points=[1 << 16, 1 << 20], repeats=2)
+    assert [r["bytes"] for r in rep.rows] == [1 << 16, 1 << 20]
+    assert all(r["rate_gbps"] > 0 for r in rep.rows)
+    back = run_backend_comparison(pixels=1 << 16, n_surfaces=4, repeats=1)
+    assert {r["backend"] for r in back.rows} == {"cuda", "cuda-batched"}
