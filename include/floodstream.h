@@ -198,6 +198,11 @@ int fs_time_h2d(uint64_t bytes, int reps, int pinned, double *us_mean, double *u
 int fs_synth_host(uint8_t *out, uint64_t seed, uint32_t width, uint32_t height, uint64_t row0,
                   uint64_t rows, uint64_t mask_index, uint32_t members, double eps,
                   int threads);
+/* The same bytes generated on the device: `out` may be device memory (written in
+ * place) or host memory, pinned or pageable (generated in device chunks and copied);
+ * for producing large inputs (e.g. 64 x 32768^2) at copy speed.                      */
+int fs_synth_gpu(uint8_t *out, uint64_t seed, uint32_t width, uint32_t height, uint64_t row0,
+                 uint64_t rows, uint64_t mask_index, uint32_t members, double eps);
 
 #ifdef __cplusplus
 }

@@ -92,6 +92,8 @@ _SIGNATURES = {
     "fs_time_h2d": [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "fs_synth_host": [_vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
                       C.c_uint64, C.c_uint32, C.c_double, C.c_int],
+    "fs_synth_gpu": [_vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
+                     C.c_uint64, C.c_uint32, C.c_double],
 }
 
 EXPORTED_SYMBOLS = ("fs_last_error",) + tuple(_SIGNATURES)

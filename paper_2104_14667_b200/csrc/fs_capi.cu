@@ -1277,4 +1277,47 @@ int fs_synth_host(uint8_t *out, uint64_t seed, uint32_t width, uint32_t height, 
   return FS_OK;
 }
 
+
+// synthetic masks generated on the device (same bytes as fs_synth_host), written to any
+// destination the CUDA runtime can address: device memory directly, host memory
+// (pinned or pageable) through a device chunk + copy.
+int fs_synth_gpu(uint8_t *out, uint64_t seed, uint32_t width, uint32_t height, uint64_t row0,
+                 uint64_t rows, uint64_t mask_index, uint32_t members, double eps) {
+  if (!out) return set_err(FS_EINVAL, "null out");
+  if (width == 0 || height == 0 || members == 0) return set_err(FS_EINVAL, "bad synth dims");
+  if (row0 + rows > height) return set_err(FS_EINVAL, "band exceeds raster");
+  ThreadCtx *c;
+  int rc = get_ctx(&c);
+  if (rc) return rc;
+  SynthParams sp;
+  sp.seed = seed;
+  sp.width = width;
+  sp.height = height;
+  sp.members = members;
+  double t = eps * 4294967296.0;
+  sp.flip_thr = t <= 0 ? 0u : (t >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)t);
+  cudaPointerAttributes at{};
+  const bool on_device = cudaPointerGetAttributes(&at, out) == cudaSuccess &&
+                         at.type == cudaMemoryTypeDevice;
+  cudaGetLastError();
+  if (on_device) {
+    CK(launch_synth_raw(out, sp, mask_index, row0, rows * width, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    return FS_OK;
+  }
+  // host destination: rows in chunks of <= 256 MiB through two device buffers
+  const uint64_t chunk_rows = std::max<uint64_t>(1, (256ull << 20) / width);
+  CK(c->a.ensure(chunk_rows * width));
+  CK(c->b.ensure(chunk_rows * width));
+  DevBuf *buf[2] = {&c->a, &c->b};
+  int i = 0;
+  for (uint64_t r = 0; r < rows; r += chunk_rows, i ^= 1) {
+    const uint64_t n = std::min(chunk_rows, rows - r);
+    CK(launch_synth_raw(buf[i]->as<uint8_t>(), sp, mask_index, row0 + r, n * width, c->s));
+    CK(cudaMemcpyAsync(out + r * width, buf[i]->p, n * width, cudaMemcpyDeviceToHost, c->s));
+  }
+  CK(cudaStreamSynchronize(c->s));
+  return FS_OK;
+}
+
 }  // extern "C"

@@ -721,6 +721,43 @@ cudaError_t launch_synth_packed(uint32_t *dst, uint64_t slot, uint64_t cap, uint
   return cudaGetLastError();
 }
 
+// Synthetic masks as raw uint8 rasters (the bytes fs_synth_host writes), 8 px per
+// thread-iteration, for generating large host inputs at copy speed.
+__global__ void k_synth_raw(uint8_t *__restrict__ dst, SynthParams sp, uint64_t mask,
+                            uint64_t row0, uint64_t pixels) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t base = row0 * sp.width;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q * 8 < pixels; q += stride) {
+    uint64_t v = 0;
+    const uint64_t p0 = q * 8;
+    const int nb = (pixels - p0) < 8 ? (int)(pixels - p0) : 8;
+    uint64_t y = (base + p0) / sp.width;
+    uint32_t x = (uint32_t)((base + p0) % sp.width);
+    for (int b = 0; b < nb; ++b) {
+      v |= (uint64_t)synth_cell(sp, mask, (uint32_t)y, x) << (8 * b);
+      if (++x == sp.width) {
+        x = 0;
+        ++y;
+      }
+    }
+    if (nb == 8 && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
+      reinterpret_cast<uint64_t *>(dst)[q] = v;
+    } else {
+      for (int b = 0; b < nb; ++b) dst[p0 + b] = (uint8_t)(v >> (8 * b));
+    }
+  }
+}
+
+cudaError_t launch_synth_raw(uint8_t *dst, const SynthParams &sp, uint64_t mask, uint64_t row0,
+                             uint64_t pixels, cudaStream_t s) {
+  if (pixels == 0) return cudaSuccess;
+  uint64_t grid = (pixels / 8 + 255) / 256 + 1;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
+  if (grid > cap) grid = cap;
+  k_synth_raw<<<(unsigned)grid, 256, 0, s>>>(dst, sp, mask, row0, pixels);
+  return cudaGetLastError();
+}
+
 // iid test rasters for the transform sweep: byte = depth 1..255 with p = 0.5, else 0
 __global__ void k_fill_random(uint8_t *__restrict__ dst, uint64_t n, uint64_t seed) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;

@@ -32,6 +32,24 @@ def synth_cells(width: int, height: int, mask: int, *, seed: int = 2104, members
     return out
 
 
+def synth_cells_gpu(width: int, height: int, mask: int, *, seed: int = 2104, members: int = 16,
+                    eps: float = 0.02, row0: int = 0, rows: int | None = None, out=None,
+                    device_ptr: int | None = None) -> np.ndarray | None:
+    """``synth_cells``'s bytes generated on the current GPU (fs_synth_gpu): into ``out``
+    (a host array, pinned or not) or straight into device memory at ``device_ptr``."""
+    rows = height - row0 if rows is None else rows
+    if device_ptr is not None:
+        N.call("fs_synth_gpu", int(device_ptr), seed, width, height, row0, rows, mask, members,
+               float(eps))
+        return None
+    if out is None:
+        out = np.empty((rows, width), dtype=np.uint8)
+    if out.dtype != np.uint8 or out.size != rows * width or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError("out must be a contiguous uint8 array of rows*width bytes")
+    N.call("fs_synth_gpu", N.ptr(out), seed, width, height, row0, rows, mask, members, float(eps))
+    return out
+
+
 def flood_surfaces(width: int, height: int, k: int, *, seed: int = 2104, members: int = 16,
                    eps: float = 0.02, first: int = 0) -> list[RasterSurface]:
     """k synthetic surfaces with ids s0000.. (mask indices first..first+k-1)."""
