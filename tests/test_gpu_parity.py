@@ -406,3 +406,28 @@ def test_transform_sweep_and_transfer_suites():
     assert all(r["rate_gbps"] > 0 for r in rep.rows)
     back = run_backend_comparison(pixels=1 << 16, n_surfaces=4, repeats=1)
     assert {r["backend"] for r in back.rows} == {"cuda", "cuda-batched"}
+
+
+# ---- config 3 at full size --------------------------------------------------------------
+
+def test_c3_scale_gram_and_clusters():
+    """1024 flood-like masks of 4096 x 4096 (config 3, device-generated): the tensor-core
+    Gram equals the CUDA-core AND+POPC engine bit for bit, Σcounts = trace(Gram), and
+    complete linkage at tau 0.8 recovers the 32 prototypes x 32 members."""
+    w = h = 4096
+    k, members = 1024, 32
+    with DeviceEnsemble(w, h, k) as ens:
+        ens.synth(0, k, seed=2104, members=members, eps=0.02)
+        c, b, r, g, fused = ens.products(engine="tc-f4")
+        g_pc = ens.gram(engine="popc")
+    assert not fused  # k > 256: separate overlap pass
+    assert np.array_equal(g, g_pc)
+    assert int(b.sum()) == w * h
+    assert int(c.sum(dtype=np.uint64)) == int(np.trace(g))
+    ids = [f"s{i:04d}" for i in range(k)]
+    sim = fs.similarity_from_gram(g)
+    clusters = fs.cluster_from_similarity(sim, ids, 0.8)
+    assert clusters == [ids[p * members:(p + 1) * members] for p in range(k // members)]
+    sub = list(range(0, k, 37))  # the host oracle on a subset of the exact matrix
+    assert fs.cluster_from_similarity(sim[np.ix_(sub, sub)], [ids[i] for i in sub], 0.8) == \
+        O.cluster(sim[np.ix_(sub, sub)], [ids[i] for i in sub], 0.8)
