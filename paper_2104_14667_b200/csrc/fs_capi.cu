@@ -1022,19 +1022,21 @@ int fs_similarity_from_gram(const int64_t *gram, uint32_t n, double *sim) {
   if (!gram || !sim) return set_err(FS_EINVAL, "null buffer");
   // analytics.py:165-171: union == 0 -> 1.0, else exact int/int true division (both
   // operands are exact in double below 2^53, so IEEE division rounds like Python's).
+  // inter and union are symmetric in (i, j), so every row is computed in full (no
+  // column-order mirror pass).
+  std::vector<int64_t> diag(n);
+  for (uint32_t i = 0; i < n; ++i) diag[i] = gram[(size_t)i * n + i];
   for (uint32_t i = 0; i < n; ++i) {
-    const int64_t gii = gram[(size_t)i * n + i];
+    const int64_t gii = diag[i];
     const int64_t *gr = gram + (size_t)i * n;
     double *sr = sim + (size_t)i * n;
-    sr[i] = 1.0;
-    for (uint32_t j = i + 1; j < n; ++j) {
+    for (uint32_t j = 0; j < n; ++j) {
       const int64_t inter = gr[j];
-      const int64_t uni = gii + gram[(size_t)j * n + j] - inter;
+      const int64_t uni = gii + diag[j] - inter;
       sr[j] = uni == 0 ? 1.0 : (double)inter / (double)uni;
     }
+    sr[i] = 1.0;
   }
-  for (uint32_t i = 0; i < n; ++i)  // mirror (row-major writes, column reads)
-    for (uint32_t j = 0; j < i; ++j) sim[(size_t)i * n + j] = sim[(size_t)j * n + i];
   return FS_OK;
 }
 
@@ -1062,20 +1064,31 @@ int fs_outlier_scores(const double *sim, uint32_t n, double *scores) {
 // only slots whose cached partner was a or b need a rescan; every other slot compares
 // its cache against the new (x, a) key.  Scores are compared first; the lexical
 // tie-break is evaluated only on exact score ties.
+//
+// Memory layout: the linkage matrix is kept dense over the live slots only.  Dead
+// columns are masked during row scans (no strided invalidation writes) and whenever
+// half of the matrix is dead it is compacted, preserving slot order, so the working
+// set shrinks geometrically (O(n^2) total compaction work) and stays cache-resident
+// late in the agglomeration when most merges happen.
 int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *id_rank,
                                 double tau, int32_t *label) {
   if (!sim || !id_rank || !label) return set_err(FS_EINVAL, "null buffer");
   if (!(tau > 0.0 && tau <= 1.0)) return set_err(FS_EINVAL, "tau must be in (0, 1]");
   constexpr uint32_t NONE = UINT32_MAX;
+  const double NEG = -std::numeric_limits<double>::infinity();
+  uint32_t m = n;                                  // matrix dimension (compacted)
   std::vector<double> L(sim, sim + (size_t)n * n);
+  std::vector<uint32_t> slot(n);                   // compacted index -> original slot
   std::vector<uint32_t> minr(id_rank, id_rank + n);
-  std::vector<int32_t> owner(n);  // surface -> slot
-  for (uint32_t i = 0; i < n; ++i) owner[i] = (int32_t)i;
-  std::vector<uint32_t> live(n);  // ascending live slots
-  for (uint32_t i = 0; i < n; ++i) live[i] = i;
+  std::vector<uint8_t> alive(n, 1);
+  std::vector<uint32_t> live(n);                   // ascending live compacted indices
+  std::vector<int32_t> owner(n);                   // surface -> original slot
+  for (uint32_t i = 0; i < n; ++i) slot[i] = live[i] = i, owner[i] = (int32_t)i;
   std::vector<double> bs(n, 0.0);
   std::vector<uint32_t> by(n, NONE);
-  // (x1, y1) before (x2, y2) at equal score
+  for (uint32_t x = 0; x < n; ++x) L[(size_t)x * n + x] = NEG;
+  // compacted indices are ordered like slots (= list positions), so they stand in for
+  // the reference's positions a, b in the tie-break
   auto tie_less = [&](uint32_t x1, uint32_t y1, uint32_t x2, uint32_t y2) {
     const uint32_t lo1 = std::min(minr[x1], minr[y1]), hi1 = std::max(minr[x1], minr[y1]);
     const uint32_t lo2 = std::min(minr[x2], minr[y2]), hi2 = std::max(minr[x2], minr[y2]);
@@ -1091,71 +1104,137 @@ int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *i
     if (s1 != s2) return s1 > s2;
     return tie_less(x1, y1, x2, y2);
   };
-  // Dead slots and the diagonal read as -inf, so a rescan is a branch-free max over
-  // one contiguous row (4 independent chains), then a pass over the exact ties.
-  const double NEG = -std::numeric_limits<double>::infinity();
-  for (uint32_t x = 0; x < n; ++x) L[(size_t)x * n + x] = NEG;
-  auto rescan = [&](uint32_t x) {
-    const double *row = L.data() + (size_t)x * n;
+  // Row scans go through per-block upper bounds (kBlk columns per block).  Linkage
+  // values only ever decrease (Lance-Williams min) or die, so a block's last exact max
+  // stays an upper bound without any update on merges; a rescan refreshes blocks in
+  // bound order until the best exact value beats every remaining bound.
+  constexpr uint32_t kBlk = 64;
+  uint32_t nblk = (m + kBlk - 1) / kBlk;
+  std::vector<double> ub;  // m x nblk
+  auto block_max = [&](uint32_t x, uint32_t blk) {
+    const double *row = L.data() + (size_t)x * m;
+    const uint8_t *al = alive.data();
+    const uint32_t y0 = blk * kBlk, y1 = std::min(m, y0 + kBlk);
     double m0 = NEG, m1 = NEG, m2 = NEG, m3 = NEG;
-    uint32_t y = 0;
-    for (; y + 4 <= n; y += 4) {
-      m0 = row[y] > m0 ? row[y] : m0;
-      m1 = row[y + 1] > m1 ? row[y + 1] : m1;
-      m2 = row[y + 2] > m2 ? row[y + 2] : m2;
-      m3 = row[y + 3] > m3 ? row[y + 3] : m3;
+    uint32_t y = y0;
+    for (; y + 4 <= y1; y += 4) {
+      const double v0 = al[y] ? row[y] : NEG, v1 = al[y + 1] ? row[y + 1] : NEG;
+      const double v2 = al[y + 2] ? row[y + 2] : NEG, v3 = al[y + 3] ? row[y + 3] : NEG;
+      m0 = v0 > m0 ? v0 : m0;
+      m1 = v1 > m1 ? v1 : m1;
+      m2 = v2 > m2 ? v2 : m2;
+      m3 = v3 > m3 ? v3 : m3;
     }
-    for (; y < n; ++y) m0 = row[y] > m0 ? row[y] : m0;
-    const double m = std::max(std::max(m0, m1), std::max(m2, m3));
+    for (; y < y1; ++y) {
+      const double v = al[y] ? row[y] : NEG;
+      m0 = v > m0 ? v : m0;
+    }
+    return std::max(std::max(m0, m1), std::max(m2, m3));
+  };
+  auto init_bounds = [&]() {
+    nblk = (m + kBlk - 1) / kBlk;
+    ub.assign((size_t)m * nblk, NEG);
+    for (uint32_t x = 0; x < m; ++x)
+      for (uint32_t k2 = 0; k2 < nblk; ++k2) ub[(size_t)x * nblk + k2] = block_max(x, k2);
+  };
+  std::vector<uint8_t> exact;  // per block: bound refreshed in this rescan
+  auto rescan = [&](uint32_t x) {
+    double *u = ub.data() + (size_t)x * nblk;
+    exact.assign(nblk, 0);
+    double best = NEG;
+    for (;;) {  // refresh the highest stale bound until it cannot beat `best`
+      uint32_t top = NONE;
+      for (uint32_t k2 = 0; k2 < nblk; ++k2)
+        if (!exact[k2] && (top == NONE || u[k2] > u[top])) top = k2;
+      if (top == NONE || u[top] < best || u[top] == NEG) break;
+      u[top] = block_max(x, top);
+      exact[top] = 1;
+      best = std::max(best, u[top]);
+    }
     uint32_t arg = NONE;
-    if (m >= tau) {
-      for (uint32_t z = 0; z < n; ++z)
-        if (row[z] == m && (arg == NONE || tie_less(x, z, x, arg))) arg = z;
+    if (best >= tau) {
+      // every block that may hold `best` has an exact bound now (stale ones are < best)
+      const double *row = L.data() + (size_t)x * m;
+      for (uint32_t k2 = 0; k2 < nblk; ++k2) {
+        if (!exact[k2] || u[k2] != best) continue;
+        const uint32_t y1 = std::min(m, (k2 + 1) * kBlk);
+        for (uint32_t z = k2 * kBlk; z < y1; ++z)
+          if (alive[z] && row[z] == best && (arg == NONE || tie_less(x, z, x, arg))) arg = z;
+      }
     }
-    bs[x] = m;
+    bs[x] = best;
     by[x] = arg;
   };
-  for (uint32_t x = 0; x < n; ++x) rescan(x);
+  auto compact = [&]() {
+    const uint32_t m2 = (uint32_t)live.size();
+    std::vector<uint32_t> newidx(m, NONE);
+    for (uint32_t c = 0; c < m2; ++c) newidx[live[c]] = c;
+    std::vector<double> L2((size_t)m2 * m2);
+    for (uint32_t r = 0; r < m2; ++r) {
+      const double *src = L.data() + (size_t)live[r] * m;
+      double *dst = L2.data() + (size_t)r * m2;
+      for (uint32_t c = 0; c < m2; ++c) dst[c] = src[live[c]];
+    }
+    std::vector<uint32_t> slot2(m2), minr2(m2), by2(m2);
+    std::vector<double> bs2(m2);
+    for (uint32_t c = 0; c < m2; ++c) {
+      const uint32_t o = live[c];
+      slot2[c] = slot[o];
+      minr2[c] = minr[o];
+      bs2[c] = bs[o];
+      by2[c] = by[o] == NONE ? NONE : newidx[by[o]];
+    }
+    L.swap(L2);
+    slot.swap(slot2);
+    minr.swap(minr2);
+    bs.swap(bs2);
+    by.swap(by2);
+    alive.assign(m2, 1);
+    for (uint32_t c = 0; c < m2; ++c) live[c] = c;
+    m = m2;
+    init_bounds();
+  };
+  init_bounds();
+  for (uint32_t x = 0; x < m; ++x) rescan(x);
   while (live.size() > 1) {
     uint32_t gx = NONE;
     for (uint32_t x : live)
       if (by[x] != NONE && (gx == NONE || better(bs[x], x, by[x], bs[gx], gx, by[gx]))) gx = x;
     if (gx == NONE) break;
     const uint32_t a = std::min(gx, by[gx]), b = std::max(gx, by[gx]);  // b merges into a
-    double *ra = L.data() + (size_t)a * n;
-    const double *rb = L.data() + (size_t)b * n;
+    double *ra = L.data() + (size_t)a * m;
+    const double *rb = L.data() + (size_t)b * m;
     for (uint32_t y : live) {
       if (y == a || y == b) continue;
       const double v = std::min(ra[y], rb[y]);
       ra[y] = v;
-      L[(size_t)y * n + a] = v;
+      L[(size_t)y * m + a] = v;
     }
     minr[a] = std::min(minr[a], minr[b]);
+    alive[b] = 0;
     live.erase(std::lower_bound(live.begin(), live.end(), b));
-    for (uint32_t y = 0; y < n; ++y) {
-      L[(size_t)b * n + y] = NEG;
-      L[(size_t)y * n + b] = NEG;
-    }
+    const int32_t sa = (int32_t)slot[a], sb = (int32_t)slot[b];
     for (uint32_t i = 0; i < n; ++i)
-      if (owner[i] == (int32_t)b) owner[i] = (int32_t)a;
+      if (owner[i] == sb) owner[i] = sa;
     rescan(a);
     for (uint32_t x : live) {
       if (x == a) continue;
       if (by[x] == a || by[x] == b) {
         rescan(x);
       } else {
-        const double v = L[(size_t)x * n + a];
+        const double v = L[(size_t)x * m + a];
         if (v >= tau && better(v, x, a, bs[x], x, by[x])) {
           bs[x] = v;
           by[x] = a;
         }
       }
     }
+    if (m > 64 && live.size() * 2 <= m) compact();
   }
   // label = position of the owning slot in the surviving list
   std::vector<int32_t> pos(n, -1);
   int32_t p = 0;
-  for (uint32_t x : live) pos[x] = p++;
+  for (uint32_t x : live) pos[slot[x]] = p++;
   for (uint32_t i = 0; i < n; ++i) label[i] = pos[owner[i]];
   return FS_OK;
 }
