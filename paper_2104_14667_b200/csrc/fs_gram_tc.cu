@@ -475,6 +475,240 @@ __global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Off-diagonal 256 x 256 tiles on a CTA PAIR: tcgen05.mma.cta_group::2.kind::mxf4.
+//
+// A single-CTA 256 x 256 FP4 tile does not fit TMEM (2 x 256 f32 accumulator columns
+// leave no room for the scale factors) and its SMEM traffic per MAC is high (both
+// A halves read the whole 256-row B operand).  On a pair, CTA r (cluster rank r) owns
+// rows [128 r, 128 r + 128) of panel I (its A half) and of panel J (its B half): it
+// loads and expands only those 256 raw rows, the leader's MMA (M = 256, N = 256,
+// K = 64) reads A and B halves from both CTAs' SMEM at the same offsets, and CTA r's
+// TMEM holds D rows [128 r, 128 r + 128) x 256 columns.  Per CTA and 256-px K stage:
+// 512 MMA cycles against ~576 cycles of SMEM traffic (expansion writes 32 KB, UMMA
+// reads 32 KB, raw reads 8 KB), i.e. near the tensor-pipe bound at 2x the int8 rate.
+//
+// Synchronisation: raw ring per CTA (TMA -> local expanders); operand stage s is
+// "full" on the LEADER's barrier once all 8 expander warps of both CTAs arrived
+// (remote arrive through mapa for rank 1); the leader's tcgen05.commit multicasts
+// "empty" and finally "tmem_full" to both CTAs.
+// ---------------------------------------------------------------------------
+constexpr int kPairThreads = 192;  // w0: TMEM alloc + MMA (leader); w1..4: expanders + epilogue; w5: TMA
+constexpr int kPairDepth = 2;      // raw units in flight per CTA
+constexpr int kPairRawUnit = 2 * 128 * 128;  // A half + B half, 1024 px (128 B) per row
+constexpr int kPairStageBytes = 2 * 128 * 128;  // A + B operand halves, 256 px per row
+constexpr int kPairStages = 4;
+constexpr int kPairSmemBytes = kPairDepth * kPairRawUnit + kPairStages * kPairStageBytes + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// arrive on the barrier at the same SMEM offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t *bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(ptx::smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// wait with cluster-scope acquire (arrivals come from the peer CTA too)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  const uint32_t addr = ptx::smem_u32(bar);
+  uint32_t done = 0;
+  uint64_t spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;"
+        "\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) break;
+    if (++spins > (1ull << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void mma_mxf4_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accum, uint32_t sfa, uint32_t sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;"
+      "\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(ptx::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
+    k_gram_pair_f4(const __grid_constant__ CUtensorMap tm, uint32_t npanels, uint32_t kchunks,
+                   uint64_t units_per_chunk, uint64_t total_units, int32_t *__restrict__ partial) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+  const uint32_t pad = (1024u - (raw_addr & 1023u)) & 1023u;
+  uint8_t *smem = smem_raw + pad;
+  const uint32_t raw_base = raw_addr + pad;
+  const uint32_t op_base = raw_base + kPairDepth * kPairRawUnit;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kPairDepth * kPairRawUnit +
+                                                kPairStages * kPairStageBytes);
+  uint64_t *empty = full + kPairStages;
+  uint64_t *raw_full = empty + kPairStages;
+  uint64_t *raw_empty = raw_full + kPairDepth;
+  uint64_t *tmem_full = raw_empty + kPairDepth;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const uint32_t pair = blockIdx.x >> 1;
+  const uint32_t tile = pair / kchunks;
+  const uint32_t kc = pair % kchunks;
+  uint32_t I = 0, t = tile;
+  while (t >= npanels - 1 - I) {
+    t -= npanels - 1 - I;
+    ++I;
+  }
+  const uint32_t J = I + 1 + t;
+  const uint64_t u0 = (uint64_t)kc * units_per_chunk;
+  const uint64_t u1 = min(u0 + units_per_chunk, total_units);
+  const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
+  constexpr int kSub = 4;  // 256-px operand stages per 1024-px raw unit
+  const int nst = nunits * kSub;
+
+  if (tid == 0) {
+    ptx::prefetch_tmap(&tm);
+    for (int q = 0; q < kPairStages; ++q) {
+      ptx::mbar_init(&full[q], 8);  // 4 expander warps x 2 CTAs (leader's copy is used)
+      ptx::mbar_init(&empty[q], 1);
+    }
+    for (int q = 0; q < kPairDepth; ++q) {
+      ptx::mbar_init(&raw_full[q], 1);
+      ptx::mbar_init(&raw_empty[q], 4);
+    }
+    ptx::mbar_init(tmem_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     ptx::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // block scales = 1.0 in both CTAs' scale-factor columns
+  if (warp >= 1 && warp <= 4) {
+    const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
+    tmem_st16(tmem + lanes + kSfCol, kSfOnes);
+    tmem_st16(tmem + lanes + kSfCol + 16, kSfOnes);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  cluster_sync_all();  // barrier inits + scale factors visible pair-wide
+  fence_after();
+
+  if (warp == 0) {
+    if (rank == 0 && lane == 0 && nst > 0) {
+      constexpr uint32_t idesc = idesc_mxf4(256, 256);
+      const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 16;
+      for (int j = 0; j < nst; ++j) {
+        const int s = j % kPairStages;
+        mbar_wait_cluster(&full[s], (uint32_t)((j / kPairStages) & 1));
+        fence_after();
+        const uint32_t a_base = op_base + s * kPairStageBytes;
+        const uint32_t b_base = a_base + 128 * 128;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          mma_mxf4_pair(tmem, sw128_desc(a_base + ks * 32), sw128_desc(b_base + ks * 32), idesc,
+                        (j > 0 || ks > 0) ? 1u : 0u, sfa, sfb);
+        mma_commit_pair(&empty[s]);
+      }
+      mma_commit_pair(tmem_full);
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    if (lane == 0) {
+      for (int u = 0; u < nunits; ++u) {
+        const int ru = u % kPairDepth;
+        if (u >= kPairDepth) ptx::mbar_wait(&raw_empty[ru], (uint32_t)(((u / kPairDepth) - 1) & 1));
+        const int c2 = (int)(u0 + (uint64_t)u);
+        ptx::mbar_arrive_expect_tx(&raw_full[ru], kPairRawUnit);
+        uint8_t *dst = smem + ru * kPairRawUnit;
+        ptx::tma_load_3d(dst, &tm, 0, (int)(I * 256 + rank * 128), c2, &raw_full[ru]);
+        ptx::tma_load_3d(dst + 128 * 128, &tm, 0, (int)(J * 256 + rank * 128), c2, &raw_full[ru]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== expanders: thread t expands row t of the A half and of the B half =====
+    const uint32_t rr = (uint32_t)(tid - 32);
+    const uint32_t sw = rr & 7u;
+    for (int j = 0; j < nst; ++j) {
+      const int u = j / kSub, sub = j % kSub;
+      const int ru = u % kPairDepth;
+      const int s = j % kPairStages;
+      if (sub == 0) ptx::mbar_wait(&raw_full[ru], (uint32_t)((u / kPairDepth) & 1));
+      if (j >= kPairStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / kPairStages) - 1) & 1));
+      const uint32_t sbase = op_base + s * kPairStageBytes;
+      const uint32_t rbase = raw_base + ru * kPairRawUnit;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t rrow = rbase + r * 128 * 128 + rr * 128;
+#pragma unroll
+        for (int hch = 0; hch < 2; ++hch) {
+          const uint32_t c = (uint32_t)(2 * sub + hch);
+          const uint4 v = ld_shared_v4(rrow + ((c ^ sw) << 4));
+          expand_row_f4(sbase + r * 128 * 128, rr, 4u * hch, v);
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_cluster(&full[s], 0);
+        if (sub == kSub - 1) ptx::mbar_arrive(&raw_empty[ru]);
+      }
+    }
+    // ===== epilogue: this CTA's 128 rows x 256 columns of D =====
+    const uint32_t q = (uint32_t)(warp & 3);
+    int32_t *out = partial + (uint64_t)pair * 256 * 256;
+    if (nst > 0) {
+      ptx::mbar_wait(tmem_full, 0);
+      fence_after();
+    }
+    const uint32_t row = rank * 128 + q * 32 + lane;
+    for (int c0 = 0; c0 < 256; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(tmem + ((q * 32u) << 16) + (uint32_t)c0, v);
+      if (nst == 0) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = (uint32_t)__float2int_rn(__uint_as_float(v[e]));
+      }
+      int4 *dst = reinterpret_cast<int4 *>(out + (uint64_t)row * 256 + c0);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        dst[e] = make_int4((int)v[4 * e], (int)v[4 * e + 1], (int)v[4 * e + 2], (int)v[4 * e + 3]);
+    }
+    fence_before();
+  }
+  __syncthreads();
+  cluster_sync_all();  // the leader's MMAs read this CTA's SMEM / write its TMEM
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 // Sum int32 partials over K chunks; scatter into the k x k Gram (both triangles).
 template <int PANEL>
 __global__ void k_gram_reduce(const int32_t *__restrict__ part_diag, uint32_t kc_diag,
@@ -536,6 +770,7 @@ __global__ void k_gather_slots(const uint32_t *__restrict__ packed, uint64_t cap
 
 struct Plan {
   int panel;
+  bool pair;  // off-diagonal tiles on CTA pairs (kind::mxf4, cta_group::2)
   uint32_t npanels, ndiag, noff;
   uint64_t units_diag, units_off;  // raw units along K for each tile kind
   uint32_t kc_diag, kc_off;
@@ -569,7 +804,14 @@ static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms, bool fp4) {
   // FP4 diagonal tiles accumulate in f32: a chunk (unit = 1024 px) must stay <= 2^24 px
   chunking(p.units_diag, p.ndiag, num_sms, p.kc_diag, p.upc_diag,
            fp4 ? kF4MaxChunkPx / 1024 : UINT64_MAX);
-  chunking(p.units_off, p.noff, num_sms, p.kc_off, p.upc_off);
+  p.pair = fp4 && p.panel == 256 && p.noff > 0;
+  if (p.pair) {
+    // one pair per two SMs; 1024-px units; f32 accumulation caps a chunk at 2^24 px
+    p.units_off = ntiles;
+    chunking(p.units_off, p.noff, num_sms / 2, p.kc_off, p.upc_off, kF4MaxChunkPx / 1024);
+  } else {
+    chunking(p.units_off, p.noff, num_sms, p.kc_off, p.upc_off);
+  }
   return p;
 }
 
@@ -644,6 +886,10 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
   if ((e = encode_packed_map(&tm_off, src, src_cap, row0, k, ntiles, raw_off, p.panel, 1,
                              raw_off == 16 ? 64 : 128)) != cudaSuccess)
     return e;
+  CUtensorMap tm_pair;
+  if (p.pair && (e = encode_packed_map(&tm_pair, src, src_cap, row0, k, ntiles, 32, 128, 1, 128)) !=
+                    cudaSuccess)
+    return e;
   const OverlapArgs none{};
   // one panel holds every mask: its diagonal CTAs see all masks of a pixel range and
   // also produce the overlap products (counts / histogram / RGBA) from the same tiles
@@ -665,7 +911,22 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
       e = fp4 ? launch_one<256, true, true>(tm_diag, p, part_diag, none, s)
               : launch_one<256, true>(tm_diag, p, part_diag, none, s);
     if (e != cudaSuccess) return e;
-    if ((e = launch_one<256, false>(tm_off, p, part_off, none, s)) != cudaSuccess) return e;
+    if (p.pair) {
+      if (p.kc_off > 0) {
+        static bool attr = false;
+        if (!attr) {
+          if ((e = cudaFuncSetAttribute(tc::k_gram_pair_f4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        tc::kPairSmemBytes)) != cudaSuccess)
+            return e;
+          attr = true;
+        }
+        tc::k_gram_pair_f4<<<2 * p.noff * p.kc_off, tc::kPairThreads, tc::kPairSmemBytes, s>>>(
+            tm_pair, p.npanels, p.kc_off, p.upc_off, p.units_off, part_off);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      }
+    } else if ((e = launch_one<256, false>(tm_off, p, part_off, none, s)) != cudaSuccess) {
+      return e;
+    }
   }
   if (fused) *fused = fuse_now;
   const uint64_t total = (uint64_t)(p.ndiag + p.noff) * per_tile;

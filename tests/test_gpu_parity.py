@@ -431,3 +431,21 @@ def test_c3_scale_gram_and_clusters():
     sub = list(range(0, k, 37))  # the host oracle on a subset of the exact matrix
     assert fs.cluster_from_similarity(sim[np.ix_(sub, sub)], [ids[i] for i in sub], 0.8) == \
         O.cluster(sim[np.ix_(sub, sub)], [ids[i] for i in sub], 0.8)
+
+
+@pytest.mark.parametrize("k,h,w", [(520, 30, 70), (300, 1100, 1536)])
+def test_gram_pair_kernel_multi_panel(k, h, w):
+    """k > 256: off-diagonal 256 x 256 tiles run on CTA pairs (cta_group::2, mxf4);
+    several panels and many K chunks against the CUDA-core engine and the oracle."""
+    rng = np.random.default_rng(k + h)
+    if h * w > 100_000:
+        cells = [synth_cells(w, h, i, members=7, eps=0.05) for i in range(k)]
+    else:
+        cells = [(rng.random((h, w)) < rng.uniform(0.05, 0.95)).astype(np.uint8) for _ in range(k)]
+    with DeviceEnsemble(w, h, k) as ens:
+        ens.upload(cells)
+        got = ens.gram(engine="tc-f4")
+        ref = ens.gram(engine="popc")
+    assert np.array_equal(got, ref)
+    if h * w <= 100_000:
+        assert np.array_equal(got, O.gram(cells))
