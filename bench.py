@@ -481,6 +481,9 @@ def main():
 
     sh = ShardedEnsemble(width, height, k)
     row0, rows = sh.row0, sh.rows
+    # frames in flight = host-analytics threads: the O(k^2) linkage at k = 1024 takes
+    # longer than the device frame, so more frames overlap it
+    depth = 3 if k <= 256 else 6
     P_band = rows * width
     ens = sh.ens
     ens.synth(0, k, seed=2104, members=members, eps=eps)
@@ -508,7 +511,7 @@ def main():
 
     # ---- resident timed region: K pipelined full recomputes ---------------------------
     sh.run_frames(slots, args.warmup, tau=args.tau, engine=args.engine, ids=ids,
-                  analytics_ranks="root", keep=False)
+                  analytics_ranks="root", keep=False, depth=depth)
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -518,7 +521,7 @@ def main():
         ev0.record(stream)
         t_wall0 = time.perf_counter()
         last = sh.run_frames(slots, args.steps, tau=args.tau, engine=args.engine, ids=ids,
-                             analytics_ranks="root", keep=False)
+                             analytics_ranks="root", keep=False, depth=depth)
         ev1.record(stream)
         ev1.synchronize()
         t_wall = time.perf_counter() - t_wall0
@@ -542,7 +545,7 @@ def main():
     # ---- per-kernel roofline: CUDA-event durations on the ensemble stream, sampled in
     # extra untimed frames (reading them blocks, which would break the pipelining) ----
     sh.run_frames(slots, 6, tau=args.tau, engine=args.engine, ids=ids, analytics_ranks="none",
-                  keep=False, before_frame=sample_kernels)
+                  keep=False, before_frame=sample_kernels, depth=depth)
     sample_kernels(1)
     fused = None
     # the two stages as separate kernels (the unfused path), for the breakdown
@@ -613,11 +616,11 @@ def main():
             ens.stream(arrays, variant="2b-final", already_banded=True)
 
         sh.run_frames(slots, 1, tau=args.tau, engine=args.engine, ids=ids, maps_to_host=True,
-                      analytics_ranks="root", keep=False, before_frame=upload)  # warm-up
+                      analytics_ranks="root", keep=False, depth=depth, before_frame=upload)  # warm-up
         barrier()
         ev0.record(stream)
         res = sh.run_frames(slots, args.e2e_steps, tau=args.tau, engine=args.engine, ids=ids,
-                            maps_to_host=True, analytics_ranks="root", keep=False,
+                            maps_to_host=True, analytics_ranks="root", keep=False, depth=depth,
                             before_frame=upload)
         ev1.record(stream)
         ev1.synchronize()

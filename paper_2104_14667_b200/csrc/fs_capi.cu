@@ -1082,8 +1082,8 @@ int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *i
   std::vector<uint32_t> minr(id_rank, id_rank + n);
   std::vector<uint8_t> alive(n, 1);
   std::vector<uint32_t> live(n);                   // ascending live compacted indices
-  std::vector<int32_t> owner(n);                   // surface -> original slot
-  for (uint32_t i = 0; i < n; ++i) slot[i] = live[i] = i, owner[i] = (int32_t)i;
+  std::vector<std::vector<uint32_t>> members(n);   // original slot -> its surfaces
+  for (uint32_t i = 0; i < n; ++i) slot[i] = live[i] = i, members[i].assign(1, i);
   std::vector<double> bs(n, 0.0);
   std::vector<uint32_t> by(n, NONE);
   for (uint32_t x = 0; x < n; ++x) L[(size_t)x * n + x] = NEG;
@@ -1213,16 +1213,18 @@ int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *i
     minr[a] = std::min(minr[a], minr[b]);
     alive[b] = 0;
     live.erase(std::lower_bound(live.begin(), live.end(), b));
-    const int32_t sa = (int32_t)slot[a], sb = (int32_t)slot[b];
-    for (uint32_t i = 0; i < n; ++i)
-      if (owner[i] == sb) owner[i] = sa;
+    {  // b's surfaces now belong to a (member lists: O(|b|) per merge)
+      auto &ma = members[slot[a]], &mb = members[slot[b]];
+      ma.insert(ma.end(), mb.begin(), mb.end());
+      mb.clear();
+    }
     rescan(a);
     for (uint32_t x : live) {
       if (x == a) continue;
       if (by[x] == a || by[x] == b) {
         rescan(x);
       } else {
-        const double v = L[(size_t)x * m + a];
+        const double v = ra[x];  // = L[x][a]: row a was just written for every live x
         if (v >= tau && better(v, x, a, bs[x], x, by[x])) {
           bs[x] = v;
           by[x] = a;
@@ -1232,10 +1234,11 @@ int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *i
     if (m > 64 && live.size() * 2 <= m) compact();
   }
   // label = position of the owning slot in the surviving list
-  std::vector<int32_t> pos(n, -1);
   int32_t p = 0;
-  for (uint32_t x : live) pos[slot[x]] = p++;
-  for (uint32_t i = 0; i < n; ++i) label[i] = pos[owner[i]];
+  for (uint32_t x : live) {
+    for (uint32_t i : members[slot[x]]) label[i] = p;
+    ++p;
+  }
   return FS_OK;
 }
 

@@ -36,8 +36,8 @@ namespace fs {
 
 namespace tc {
 
-constexpr int kThreads = 192;  // w0: TMEM alloc + MMA; w1..4: expanders + epilogue; w5: TMA
-constexpr int kThreadsFused = 320;  // + w6..9: per-pixel counters (fused overlap pass)
+// warp roles (Cfg::k*Warp*): w0 TMEM alloc + MMA; w1..kExpWarps expanders + epilogue;
+// then the TMA warp; then (FUSE) 4 per-pixel counter warps of the fused overlap pass
 constexpr int kFuseBins = 288;      // SMEM histogram / RGBA table (k <= 256 -> <= 257 bins)
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kRawDepth = 2;
@@ -186,8 +186,15 @@ struct Cfg {
   static constexpr int kDepth = FUSE ? 4 : kRawDepth;
   static constexpr int kExtraBytes = FUSE ? (4 * 32 * kTileTb * 4 + 2 * kFuseBins * 4) : 0;
   static constexpr int kBudget = FUSE ? (232448 - 1024 - 256) : kSmemBudget;
-  static constexpr int kRowsPerThread = PANEL / 128;  // per region, 128 expander threads
   static constexpr int kRegions = DIAG ? 1 : 2;
+  // 8 expander warps when there are >= 256 operand rows (latency hiding: each thread's
+  // loads -> expand -> stores chain is short), else 4
+  static constexpr int kExpWarps = (PANEL * kRegions >= 256) ? 8 : 4;
+  static constexpr int kExpThreads = 32 * kExpWarps;
+  static constexpr int kRowsPerThread = PANEL * kRegions / kExpThreads;  // all regions
+  static constexpr int kTmaWarp = kExpWarps + 1;
+  static constexpr int kCntWarp0 = kExpWarps + 2;
+  static constexpr int kThreadsTotal = 32 * (kExpWarps + 2 + (FUSE ? 4 : 0));
   static constexpr int kRawRow = (PANEL == 256 && !DIAG) ? 64 : 128;  // raw bytes/row/unit
   static constexpr int kRawPerStage = FP4 ? 32 : 16;  // raw bytes per row per K stage
   static constexpr int kStagesPerUnit = kRawRow / kRawPerStage;
@@ -208,7 +215,7 @@ struct Cfg {
 };
 
 template <int PANEL, bool DIAG, bool FP4, bool FUSE>
-__global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
+__global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE>::kThreadsTotal, 1)
     k_gram_tc(const __grid_constant__ CUtensorMap tm, uint32_t npanels, uint32_t kchunks,
               uint64_t units_per_chunk, uint64_t total_units, int32_t *__restrict__ partial,
               const OverlapArgs ov) {
@@ -258,19 +265,19 @@ __global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
   if (tid == 0) {
     ptx::prefetch_tmap(&tm);
     for (int s = 0; s < C::kStages; ++s) {
-      ptx::mbar_init(&full[s], 128);
+      ptx::mbar_init(&full[s], C::kExpThreads);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kRawDepth; ++s) {
       ptx::mbar_init(&raw_full[s], 1);
-      ptx::mbar_init(&raw_empty[s], FUSE ? 128 + 32 : 128);
+      ptx::mbar_init(&raw_empty[s], FUSE ? C::kExpThreads + 32 : C::kExpThreads);
     }
     ptx::mbar_init(tmem_full, 1);
     ptx::fence_mbar_init();
   }
   const bool lut_sh = FUSE && ov.rgba != nullptr;
-  if (FUSE && tid >= kThreads) {
-    for (int i = tid - kThreads; i < kFuseBins; i += kThreadsFused - kThreads) {
+  if (FUSE && warp >= C::kCntWarp0) {
+    for (int i = tid - 32 * C::kCntWarp0; i < kFuseBins; i += 128) {
       sh_hist[i] = 0;
       sh_lut[i] = lut_sh && (uint32_t)i < ov.nbins ? rgba_word(i, ov.n_inputs, ov.lut) : 0u;
     }
@@ -337,7 +344,7 @@ __global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
       mma_commit(tmem_full);
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == C::kTmaWarp) {
     // ===== TMA loader: one contiguous [PANEL rows][raw row] box per region per unit =====
     if (lane == 0) {
       constexpr int kUnitsPerTile = 128 / C::kRawRow;
@@ -357,11 +364,11 @@ __global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (FUSE && warp >= 6) {
+  } else if (FUSE && warp >= C::kCntWarp0) {
     // ===== counters: the fused overlap pass over the same raw tiles =====
     // warp cw takes units cw, cw+4, ...: lane = word of the 1024-px tile, a bit-sliced
     // adder over all PANEL mask rows, then the tile epilogue (histogram, counts, RGBA).
-    const int cw = warp - 6;
+    const int cw = warp - C::kCntWarp0;
     uint32_t off[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -403,32 +410,48 @@ __global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
       if (j >= C::kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / C::kStages) - 1) & 1));
       const uint32_t sbase = op_base + s * C::kStageBytes;
       const uint32_t rbase = raw_base + ru * C::kRawUnitBytes;
+      // all raw loads of this stage first, then the expansion stores: the shared-memory
+      // accesses are volatile asm (ordered), so interleaving them would serialise every
+      // load's latency behind the previous row's stores
+      constexpr int kPer = FP4 ? 2 : 1;  // raw 16-B chunks per row per stage
+      uint4 v[C::kRowsPerThread * kPer];
 #pragma unroll
-      for (int r = 0; r < C::kRegions; ++r)
+      for (int m = 0; m < C::kRowsPerThread; ++m) {
+        const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
+        const uint32_t r = idx / PANEL, rr = idx % PANEL;
+        const uint32_t sw = C::kRawRow == 128 ? (rr & 7u) : ((rr >> 1) & 3u);
+        const uint32_t rrow = rbase + r * PANEL * C::kRawRow + rr * C::kRawRow;
+        if (FP4) {
 #pragma unroll
-        for (int m = 0; m < C::kRowsPerThread; ++m) {
-          const uint32_t rr = ptid + m * 128;
-          const uint32_t sw = C::kRawRow == 128 ? (rr & 7u) : ((rr >> 1) & 3u);
-          const uint32_t rrow = rbase + r * PANEL * C::kRawRow + rr * C::kRawRow;
-          if (FP4) {
-            // 32 raw bytes (256 px) -> the whole 128-B operand row
-#pragma unroll
-            for (int hch = 0; hch < 2; ++hch) {
-              const uint32_t u = (uint32_t)(2 * sub + hch);
-              const uint4 v = ld_shared_v4(rrow + ((u ^ sw) << 4));
-              expand_row_f4(sbase + r * C::kRegionBytes, rr, 4u * hch, v);
-            }
-          } else {
-            const uint4 v = ld_shared_v4(rrow + (((uint32_t)sub ^ sw) << 4));
-            expand_row(sbase + r * C::kRegionBytes, rr, v);
+          for (int hch = 0; hch < 2; ++hch) {
+            const uint32_t u = (uint32_t)(2 * sub + hch);
+            v[m * kPer + hch] = ld_shared_v4(rrow + ((u ^ sw) << 4));
           }
+        } else {
+          v[m] = ld_shared_v4(rrow + (((uint32_t)sub ^ sw) << 4));
         }
+      }
+#pragma unroll
+      for (int m = 0; m < C::kRowsPerThread; ++m) {
+        const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
+        const uint32_t r = idx / PANEL, rr = idx % PANEL;
+        if (FP4) {
+          // 32 raw bytes (256 px) -> the whole 128-B operand row
+#pragma unroll
+          for (int hch = 0; hch < 2; ++hch)
+            expand_row_f4(sbase + r * C::kRegionBytes, rr, 4u * hch, v[m * kPer + hch]);
+        } else {
+          expand_row(sbase + r * C::kRegionBytes, rr, v[m]);
+        }
+      }
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&full[s]);
       if (sub == C::kStagesPerUnit - 1) ptx::mbar_arrive(&raw_empty[ru]);
     }
     // ===== epilogue: TMEM -> registers -> int32 partial tile =====
     const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp
+    constexpr int kColGroups = C::kExpWarps / 4;  // warps sharing a lane quarter split columns
+    const int cg = (warp - 1) / 4;
     int32_t *out = partial + (uint64_t)blockIdx.x * PANEL * PANEL;
     if (nst > 0) {
       ptx::mbar_wait(tmem_full, 0);
@@ -439,7 +462,7 @@ __global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
       const uint32_t row = h * 128 + q * 32 + lane;
       const bool lower_diag = DIAG && PANEL == 256 && h == 1;
       const int c_begin = lower_diag ? 128 : 0;
-      for (int c0 = c_begin; c0 < PANEL; c0 += 32) {
+      for (int c0 = c_begin + 32 * cg; c0 < PANEL; c0 += 32 * kColGroups) {
         uint32_t v[32];
         const uint32_t col =
             lower_diag ? (256u + (uint32_t)(c0 - 128)) : (uint32_t)(h * PANEL + c0);
@@ -460,10 +483,10 @@ __global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
     fence_before();
   }
   __syncthreads();
-  if (FUSE && tid >= kThreads && ov.bins != nullptr) {
-    for (uint32_t i = tid - kThreads; i < ov.nbins; i += kThreadsFused - kThreads)
+  if (FUSE && warp >= C::kCntWarp0 && ov.bins != nullptr) {
+    for (uint32_t i = tid - 32 * C::kCntWarp0; i < ov.nbins; i += 128)
       if (sh_hist[i]) atomicAdd(ov.bins + i, (unsigned long long)sh_hist[i]);
-    if (blockIdx.x == 0 && tid == kThreads) {
+    if (blockIdx.x == 0 && tid == 32 * C::kCntWarp0) {
       const uint64_t pad = total_units * 1024 - ov.pixels;  // padding counted in bin 0
       if (pad) atomicAdd(ov.bins, (unsigned long long)(0ull - pad));
     }
@@ -493,7 +516,8 @@ __global__ void __launch_bounds__(FUSE ? kThreadsFused : kThreads, 1)
 // (remote arrive through mapa for rank 1); the leader's tcgen05.commit multicasts
 // "empty" and finally "tmem_full" to both CTAs.
 // ---------------------------------------------------------------------------
-constexpr int kPairThreads = 192;  // w0: TMEM alloc + MMA (leader); w1..4: expanders + epilogue; w5: TMA
+constexpr int kPairThreads = 320;  // w0: TMEM alloc + MMA (leader); w1..8: expanders + epilogue; w9: TMA
+constexpr int kPairExpWarps = 8;   // thread t < 128 expands A-half row t, t >= 128 B-half row t - 128
 constexpr int kPairDepth = 2;      // raw units in flight per CTA
 constexpr int kPairRawUnit = 2 * 128 * 128;  // A half + B half, 1024 px (128 B) per row
 constexpr int kPairStageBytes = 2 * 128 * 128;  // A + B operand halves, 256 px per row
@@ -513,7 +537,10 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t *bar, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(ptx::smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  // plain remote arrive (default .release.cta, like CUTLASS's ClusterBarrier::arrive):
+  // the .release.cluster form costs a MEMBAR.ALL.GPU per stage; the operand writes
+  // are already ordered for the tensor core by fence.proxy.async before this arrive
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 // wait with cluster-scope acquire (arrivals come from the peer CTA too)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
@@ -585,12 +612,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   if (tid == 0) {
     ptx::prefetch_tmap(&tm);
     for (int q = 0; q < kPairStages; ++q) {
-      ptx::mbar_init(&full[q], 8);  // 4 expander warps x 2 CTAs (leader's copy is used)
+      ptx::mbar_init(&full[q], 2 * kPairExpWarps);  // expander warps of both CTAs (leader's copy)
       ptx::mbar_init(&empty[q], 1);
     }
     for (int q = 0; q < kPairDepth; ++q) {
       ptx::mbar_init(&raw_full[q], 1);
-      ptx::mbar_init(&raw_empty[q], 4);
+      ptx::mbar_init(&raw_empty[q], kPairExpWarps);
     }
     ptx::mbar_init(tmem_full, 1);
     ptx::fence_mbar_init();
@@ -634,7 +661,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       mma_commit_pair(tmem_full);
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == kPairExpWarps + 1) {
     if (lane == 0) {
       for (int u = 0; u < nunits; ++u) {
         const int ru = u % kPairDepth;
@@ -648,8 +675,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     }
     __syncwarp();
   } else {
-    // ===== expanders: thread t expands row t of the A half and of the B half =====
-    const uint32_t rr = (uint32_t)(tid - 32);
+    // ===== expanders: thread t expands row t % 128 of the A (t < 128) or B half =====
+    const uint32_t et = (uint32_t)(tid - 32);
+    const uint32_t reg = et >> 7, rr = et & 127u;
     const uint32_t sw = rr & 7u;
     for (int j = 0; j < nst; ++j) {
       const int u = j / kSub, sub = j % kSub;
@@ -657,18 +685,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const int s = j % kPairStages;
       if (sub == 0) ptx::mbar_wait(&raw_full[ru], (uint32_t)((u / kPairDepth) & 1));
       if (j >= kPairStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / kPairStages) - 1) & 1));
-      const uint32_t sbase = op_base + s * kPairStageBytes;
-      const uint32_t rbase = raw_base + ru * kPairRawUnit;
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint32_t rrow = rbase + r * 128 * 128 + rr * 128;
-#pragma unroll
-        for (int hch = 0; hch < 2; ++hch) {
-          const uint32_t c = (uint32_t)(2 * sub + hch);
-          const uint4 v = ld_shared_v4(rrow + ((c ^ sw) << 4));
-          expand_row_f4(sbase + r * 128 * 128, rr, 4u * hch, v);
-        }
-      }
+      const uint32_t rrow = raw_base + ru * kPairRawUnit + reg * 128 * 128 + rr * 128;
+      const uint4 v0 = ld_shared_v4(rrow + ((((uint32_t)(2 * sub)) ^ sw) << 4));
+      const uint4 v1 = ld_shared_v4(rrow + ((((uint32_t)(2 * sub + 1)) ^ sw) << 4));
+      const uint32_t obase = op_base + s * kPairStageBytes + reg * 128 * 128;
+      expand_row_f4(obase, rr, 0u, v0);
+      expand_row_f4(obase, rr, 4u, v1);
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -677,14 +699,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
     }
     // ===== epilogue: this CTA's 128 rows x 256 columns of D =====
-    const uint32_t q = (uint32_t)(warp & 3);
+    const uint32_t q = (uint32_t)(warp & 3);     // TMEM lane quarter of this warp
+    const int chalf = (warp - 1) / 4;            // warps 1..4: columns 0..127, 5..8: 128..255
     int32_t *out = partial + (uint64_t)pair * 256 * 256;
     if (nst > 0) {
       ptx::mbar_wait(tmem_full, 0);
       fence_after();
     }
     const uint32_t row = rank * 128 + q * 32 + lane;
-    for (int c0 = 0; c0 < 256; c0 += 32) {
+    for (int c0 = chalf * 128; c0 < chalf * 128 + 128; c0 += 32) {
       uint32_t v[32];
       tmem_ld32(tmem + ((q * 32u) << 16) + (uint32_t)c0, v);
       if (nst == 0) {
@@ -784,7 +807,8 @@ static void chunking(uint64_t total_units, uint32_t ntiles, int num_sms, uint32_
     upc = 0;
     return;
   }
-  uint64_t want = ((uint64_t)num_sms + ntiles - 1) / ntiles;
+  // chunks per tile: as many as keep ntiles * chunks within one wave of num_sms CTAs
+  uint64_t want = (uint64_t)num_sms / ntiles;
   if (want < 1) want = 1;
   if (want > total_units) want = total_units;
   upc = (total_units + want - 1) / want;
@@ -841,7 +865,7 @@ static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t 
     attr = true;
   }
   tc::k_gram_tc<PANEL, DIAG, FP4, FUSE>
-      <<<ntiles * kc, FUSE ? tc::kThreadsFused : tc::kThreads, C::kSmemBytes, s>>>(
+      <<<ntiles * kc, C::kThreadsTotal, C::kSmemBytes, s>>>(
           tm, p.npanels, kc, upc, units, part, ov);
   return cudaGetLastError();
 }
