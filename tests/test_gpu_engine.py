@@ -105,3 +105,36 @@ def test_analytics_engine_worker_follows_the_store():
         assert j["version"] == v and j["n_inputs"] == 6 and j["histogram"] == snap.histogram
     finally:
         eng.stop()
+
+
+def test_ingest_files_stream_into_ensemble(tmp_path):
+    """PGM (read straight into pinned staging) and PNG files decoded one batch ahead of
+    the 2b-final upload reproduce the oracle's maps and Gram."""
+    import io as _io
+
+    from PIL import Image
+
+    from paper_2104_14667_b200.ensemble import DeviceEnsemble
+    from paper_2104_14667_b200.ingest import stream_files
+    from paper_2104_14667_b200.rasters import write_pgm
+
+    w, h, k = 333, 129, 11
+    cells = [synth_cells(w, h, i, members=3, eps=0.05) for i in range(k)]
+    sources = []
+    for i, c in enumerate(cells):
+        if i % 3 == 2:
+            b = _io.BytesIO()
+            Image.fromarray(c, "L").save(b, format="PNG")
+            sources.append(b.getvalue())
+        else:
+            p = tmp_path / f"s{i}.pgm"
+            p.write_bytes(write_pgm(c))
+            sources.append(str(p))
+    with DeviceEnsemble(w, h, k + 2) as ens:
+        rep = stream_files(ens, sources, first=2, batch=4)
+        c, b, r = ens.overlap(list(range(2, k + 2)))
+        g = ens.gram(list(range(2, k + 2)), engine="tc-f4")
+    assert rep["files"] == k
+    want = O.accumulate(cells, w, h)
+    assert np.array_equal(c, want)
+    assert np.array_equal(g, O.gram(cells))
