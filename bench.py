@@ -54,7 +54,7 @@ CONFIGS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
@@ -82,7 +82,7 @@ class Clocks:
         "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80,
     }
 
-    def __init__(self, gpu_index: int, period_s: float = 0.005):
+    def __init__(self, gpu_index: int, period_s: float = 0.002):
         self.idx = gpu_index
         self.period = period_s
         self.sm: list[float] = []

@@ -1032,16 +1032,31 @@ int fs_similarity_from_gram(const int64_t *gram, uint32_t n, double *sim) {
   // column-order mirror pass).
   std::vector<int64_t> diag(n);
   for (uint32_t i = 0; i < n; ++i) diag[i] = gram[(size_t)i * n + i];
-  for (uint32_t i = 0; i < n; ++i) {
-    const int64_t gii = diag[i];
-    const int64_t *gr = gram + (size_t)i * n;
-    double *sr = sim + (size_t)i * n;
-    for (uint32_t j = 0; j < n; ++j) {
-      const int64_t inter = gr[j];
-      const int64_t uni = gii + diag[j] - inter;
-      sr[j] = uni == 0 ? 1.0 : (double)inter / (double)uni;
+  auto rows = [&](uint32_t r0, uint32_t r1) {
+    for (uint32_t i = r0; i < r1; ++i) {
+      const int64_t gii = diag[i];
+      const int64_t *gr = gram + (size_t)i * n;
+      double *sr = sim + (size_t)i * n;
+      for (uint32_t j = 0; j < n; ++j) {
+        const int64_t inter = gr[j];
+        const int64_t uni = gii + diag[j] - inter;
+        sr[j] = uni == 0 ? 1.0 : (double)inter / (double)uni;
+      }
+      sr[i] = 1.0;
     }
-    sr[i] = 1.0;
+  };
+  // rows are independent: split large matrices (k = 1024: 1M divisions) over threads
+  const uint32_t nt = n >= 512 ? std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2)) : 1u;
+  if (nt <= 1) {
+    rows(0, n);
+  } else {
+    std::vector<std::thread> ts;
+    const uint32_t per = (n + nt - 1) / nt;
+    for (uint32_t t = 0; t < nt; ++t) {
+      const uint32_t a = t * per, b = std::min(n, a + per);
+      if (a < b) ts.emplace_back(rows, a, b);
+    }
+    for (auto &th : ts) th.join();
   }
   return FS_OK;
 }
@@ -1051,7 +1066,25 @@ int fs_outlier_scores(const double *sim, uint32_t n, double *scores) {
   if (n < 2) return set_err(FS_EINVAL, "outlier scores need at least two surfaces");
   // analytics.py:237-239: builtin sum() over np.float64 = plain left-to-right adds in
   // ascending j (this TU is built without fast-math, so no reassociation/contraction).
-  for (uint32_t i = 0; i < n; ++i) {
+  // Four rows at a time, each still one left-to-right chain (the add latency of one
+  // chain hides behind the other three).  The skipped diagonal term is added as +0.0,
+  // which leaves a non-negative partial sum bit-identical.
+  uint32_t i = 0;
+  for (; i + 4 <= n; i += 4) {
+    const double *r0 = sim + (size_t)i * n, *r1 = r0 + n, *r2 = r1 + n, *r3 = r2 + n;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (uint32_t j = 0; j < n; ++j) {
+      s0 += j == i ? 0.0 : r0[j];
+      s1 += j == i + 1 ? 0.0 : r1[j];
+      s2 += j == i + 2 ? 0.0 : r2[j];
+      s3 += j == i + 3 ? 0.0 : r3[j];
+    }
+    scores[i] = 1.0 - s0 / (double)(n - 1);
+    scores[i + 1] = 1.0 - s1 / (double)(n - 1);
+    scores[i + 2] = 1.0 - s2 / (double)(n - 1);
+    scores[i + 3] = 1.0 - s3 / (double)(n - 1);
+  }
+  for (; i < n; ++i) {
     const double *r = sim + (size_t)i * n;
     double s = 0.0;
     for (uint32_t j = 0; j < i; ++j) s += r[j];
@@ -1076,10 +1109,13 @@ int fs_outlier_scores(const double *sim, uint32_t n, double *scores) {
 // half of the matrix is dead it is compacted, preserving slot order, so the working
 // set shrinks geometrically (O(n^2) total compaction work) and stays cache-resident
 // late in the agglomeration when most merges happen.
-int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *id_rank,
-                                double tau, int32_t *label) {
-  if (!sim || !id_rank || !label) return set_err(FS_EINVAL, "null buffer");
-  if (!(tau > 0.0 && tau <= 1.0)) return set_err(FS_EINVAL, "tau must be in (0, 1]");
+}  // extern "C"
+
+// One connected block of the agglomeration (see fs_cluster_complete_linkage): `sim` is
+// the n x n submatrix of the block's surfaces in ascending list order; label[i] gets
+// the block-local cluster index.
+static void linkage_block(const double *sim, uint32_t n, const uint32_t *id_rank, double tau,
+                          int32_t *label) {
   constexpr uint32_t NONE = UINT32_MAX;
   const double NEG = -std::numeric_limits<double>::infinity();
   uint32_t m = n;                                  // matrix dimension (compacted)
@@ -1244,6 +1280,66 @@ int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *i
   for (uint32_t x : live) {
     for (uint32_t i : members[slot[x]]) label[i] = p;
     ++p;
+  }
+}
+
+extern "C" {
+
+// Complete linkage of analytics.py:184-226, decomposed exactly: a merge needs every
+// member pair of the two clusters at >= tau, so every cluster is a clique of the graph
+// {(i, j): sim >= tau} and never spans two of its connected components; merges in one
+// component leave every other component's linkages untouched, and the reference's
+// global choice restricted to a component is that component's own choice (same keys:
+// score, min-id ranks, list positions in the same relative order).  Each component is
+// agglomerated on its own small submatrix — O(sum of component sizes^2) working set
+// instead of O(n^2) per merge.
+int fs_cluster_complete_linkage(const double *sim, uint32_t n, const uint32_t *id_rank,
+                                double tau, int32_t *label) {
+  if (!sim || !id_rank || !label) return set_err(FS_EINVAL, "null buffer");
+  if (!(tau > 0.0 && tau <= 1.0)) return set_err(FS_EINVAL, "tau must be in (0, 1]");
+  std::vector<uint32_t> parent(n);
+  for (uint32_t i = 0; i < n; ++i) parent[i] = i;
+  auto find = [&](uint32_t x) {
+    while (parent[x] != x) x = parent[x] = parent[parent[x]];
+    return x;
+  };
+  for (uint32_t i = 0; i < n; ++i) {
+    const double *row = sim + (size_t)i * n;
+    for (uint32_t j = i + 1; j < n; ++j)
+      if (row[j] >= tau) {
+        const uint32_t a = find(i), b = find(j);
+        if (a != b) parent[std::max(a, b)] = std::min(a, b);
+      }
+  }
+  std::vector<std::vector<uint32_t>> comp(n);  // root -> members, ascending
+  for (uint32_t i = 0; i < n; ++i) comp[find(i)].push_back(i);
+  int32_t base = 0;
+  std::vector<double> sub;
+  std::vector<uint32_t> rsub;
+  std::vector<int32_t> lsub;
+  for (uint32_t r = 0; r < n; ++r) {
+    const auto &m = comp[r];
+    if (m.empty()) continue;
+    if (m.size() == 1) {
+      label[m[0]] = base++;
+      continue;
+    }
+    const uint32_t s = (uint32_t)m.size();
+    sub.resize((size_t)s * s);
+    rsub.resize(s);
+    lsub.resize(s);
+    for (uint32_t a = 0; a < s; ++a) {
+      rsub[a] = id_rank[m[a]];
+      const double *row = sim + (size_t)m[a] * n;
+      for (uint32_t b = 0; b < s; ++b) sub[(size_t)a * s + b] = row[m[b]];
+    }
+    linkage_block(sub.data(), s, rsub.data(), tau, lsub.data());
+    int32_t mx = -1;
+    for (uint32_t a = 0; a < s; ++a) {
+      label[m[a]] = base + lsub[a];
+      mx = std::max(mx, lsub[a]);
+    }
+    base += mx + 1;
   }
   return FS_OK;
 }

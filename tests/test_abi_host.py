@@ -211,3 +211,32 @@ def test_clustering_c3_shape_blocks():
     cl = cluster_from_similarity(sim, ids, 0.8)
     assert len(cl) == 32 and all(len(c) == 32 for c in cl)
     assert cl[0] == ids[:32]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_clustering_components_with_cross_block_ties(seed):
+    """Complete linkage runs per connected component of {sim >= tau}; blocks whose
+    internal similarities tie exactly with other blocks' (and duplicated ids across
+    blocks) must still give the reference's lists."""
+    from paper_2104_14667_b200.analytics import cluster_from_similarity
+
+    rng = np.random.default_rng(77 + seed)
+    nb, m = int(rng.integers(2, 7)), int(rng.integers(1, 6))
+    k = nb * m
+    levels = np.array([0.8, 0.85, 0.9, 1.0])
+    sim = np.full((k, k), 0.1)
+    for b in range(nb):
+        blk = rng.choice(levels, (m, m))
+        blk = np.triu(blk, 1)
+        sim[b * m:(b + 1) * m, b * m:(b + 1) * m] = blk + blk.T
+    # a few bridges above tau join blocks into larger components
+    for _ in range(int(rng.integers(0, 3))):
+        i, j = rng.integers(0, k, 2)
+        if i != j:
+            sim[i, j] = sim[j, i] = 0.85
+    np.fill_diagonal(sim, 1.0)
+    perm = rng.permutation(k)
+    sim = sim[np.ix_(perm, perm)]
+    ids = [f"s{v % (k - 1 if seed % 2 else k):03d}" for v in rng.permutation(k)]
+    for tau in (0.8, 0.85, 0.9, 1.0):
+        assert cluster_from_similarity(sim, ids, tau) == O.cluster(sim, ids, tau)
