@@ -463,7 +463,7 @@ def main():
 
     from paper_2104_14667_b200 import _native as N
     from paper_2104_14667_b200.dist import ShardedEnsemble
-    from paper_2104_14667_b200.synth import synth_cells
+    from paper_2104_14667_b200.synth import synth_cells, synth_cells_gpu
 
     torch.cuda.set_device(local_rank)
     N.set_device(local_rank)
@@ -607,9 +607,9 @@ def main():
     host = h_counts = None
     if not args.no_e2e:
         host = [N.PinnedBuffer((P_band,)) for _ in range(k)]
-        for i in range(k):
-            synth_cells(width, height, i, seed=2104, members=members, eps=eps, row0=row0,
-                        rows=rows, out=host[i].array.reshape(rows, width))
+        for i in range(k):  # the generator's bytes, produced on the GPU (fs_synth_gpu)
+            synth_cells_gpu(width, height, i, seed=2104, members=members, eps=eps, row0=row0,
+                            rows=rows, out=host[i].array.reshape(rows, width))
         arrays = [h.array for h in host]
 
         def upload(_f):
