@@ -138,3 +138,18 @@ def test_ingest_files_stream_into_ensemble(tmp_path):
     want = O.accumulate(cells, w, h)
     assert np.array_equal(c, want)
     assert np.array_equal(g, O.gram(cells))
+
+
+def test_resident_engine_beyond_one_panel():
+    """A working set of 300 surfaces (> one 256-mask panel: unfused overlap + CTA-pair
+    Gram tiles) in shuffled order, then a partial swap."""
+    store = FakeStore(96, 40, 320)
+    ids_all = sorted(store.cells)
+    rng = np.random.default_rng(3)
+    with ResidentEngine(96, 40, 310) as eng:
+        ws = [ids_all[i] for i in rng.permutation(300)]
+        _check(eng.compute(1, ws, store.surface), store, ws)
+        ws2 = ws[20:] + ids_all[300:310]
+        s2 = eng.compute(2, ws2, store.surface)
+        assert s2.report["uploaded"] == 10
+        _check(s2, store, ws2)
