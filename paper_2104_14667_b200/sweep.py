@@ -217,3 +217,87 @@ def run_backend_comparison(pixels: int = 1 << 20, n_surfaces: int = 16, repeats:
     return BenchReport(suite="backends", rows=rows,
                        environment={"pixels": pixels, "surfaces": n_surfaces, "repeats": repeats},
                        csv_columns=["backend", "pixels", "surfaces", "best_s", "mpix_per_s"])
+
+
+# the paper's image sizes (bench.py:41-46 of the reference)
+DIMS = {"2k": (1856, 2208), "4k": (3712, 4416), "8k": (7424, 8832), "16k": (14848, 17664)}
+VARIANTS = ("1b-initial", "2b-initial", "1b-final", "2b-final")
+
+
+def resolve_dims(entry) -> tuple[str, int, int]:
+    """'4k', 'WxH' or (w, h) -> (label, w, h) (bench.py:167-181)."""
+    if isinstance(entry, str):
+        if entry in DIMS:
+            return (entry,) + DIMS[entry]
+        if "x" in entry:
+            try:
+                w_s, h_s = entry.lower().split("x", 1)
+                return entry, int(w_s), int(h_s)
+            except ValueError:
+                pass
+        raise BenchError(f"unknown image size {entry!r}")
+    w, h = entry
+    return f"{w}x{h}", int(w), int(h)
+
+
+def run_dual_buffer_suite(dims_list, n_list, repeats: int = 3, *, pool: int = 8,
+                          with_kernel: bool = True) -> BenchReport:
+    """The four upload strategies MEASURED on the device (the reference simulates them,
+    bench.py:231-309; the paper's Figs. 5-8): for each size, strategy and N, N rasters
+    (cycled from a pool of ``pool`` pinned host rasters) stream through the variant's
+    event DAG — H2D, bit-pack transform, per-item accumulate — and the device clock
+    gives the total.  efficiency = N x (isolated pinned copy time) / total, the paper's
+    definition; ``closed_form_us`` is the §7.1 model evaluated on the
+    measured per-item c/m/p (streaming.closed_form_times)."""
+    from .ensemble import DeviceEnsemble
+    from .streaming import closed_form_times
+    from .synth import synth_cells_gpu
+
+    if not dims_list or not n_list:
+        raise BenchError("dims and n lists must be nonempty")
+    if repeats < 1:
+        raise BenchError("repeats must be >= 1")
+    rows = []
+    for entry in dims_list:
+        label, w, h = resolve_dims(entry)
+        P = w * h
+        bufs = [N.PinnedBuffer((h, w)) for _ in range(pool)]
+        try:
+            for i, b in enumerate(bufs):
+                synth_cells_gpu(w, h, i, seed=2104, members=4, eps=0.05, out=b.array)
+            c_iso = h2d_time_us(P, reps=5, pinned=True)[1]
+            with DeviceEnsemble(w, h, 2) as ens:
+                for variant in VARIANTS:
+                    for n in n_list:
+                        if n < 1:
+                            raise BenchError("N values must be >= 1")
+                        rasters = [bufs[i % pool].array for i in range(n)]
+                        ens.stream(rasters[:min(n, 4)], variant=variant, with_kernel=with_kernel,
+                                   slot_wrap=2)  # warm-up
+                        samples, last = [], None
+                        for _ in range(repeats):
+                            last = ens.stream(rasters, variant=variant, with_kernel=with_kernel,
+                                              slot_wrap=2)
+                            samples.append(last.total_us)
+                        total = float(np.median(samples))
+                        t_dual, t_single = closed_form_times(last.copy_us, last.xform_us,
+                                                             last.kernel_us)
+                        rows.append({"dims": label, "width": w, "height": h, "variant": variant,
+                                     "n": n, "total_us": total,
+                                     "rate_gbps": n * P / total / 1000.0,
+                                     "efficiency": n * c_iso / total,
+                                     "isolated_copy_us": c_iso,
+                                     "mean_copy_us": float(np.mean(last.copy_us)),
+                                     "mean_xform_us": float(np.mean(last.xform_us)),
+                                     "mean_kernel_us": float(np.mean(last.kernel_us)),
+                                     "mean_host_us": float(np.mean(last.host_us)),
+                                     "closed_form_us": t_dual if variant.startswith("2b") else t_single,
+                                     "samples_us": samples})
+        finally:
+            for b in bufs:
+                b.free()
+    return BenchReport(suite="dual", rows=rows,
+                       environment={"device": "B200", "measured": True, "repeats": repeats,
+                                    "pool": pool, "with_kernel": with_kernel},
+                       csv_columns=["variant", "n", "width", "height", "total_us", "rate_gbps",
+                                    "efficiency"])

@@ -408,6 +408,19 @@ def test_transform_sweep_and_transfer_suites():
     assert {r["backend"] for r in back.rows} == {"cuda", "cuda-batched"}
 
 
+def test_dual_buffer_suite_measured():
+    """The paper's four strategies measured through the real event DAG (bench.py:231-309
+    schema): every (variant, N) row present, positive totals, efficiency in (0, 1.5)."""
+    from paper_2104_14667_b200.sweep import VARIANTS, run_dual_buffer_suite
+
+    rep = run_dual_buffer_suite(["96x64", (200, 30)], [3, 7], repeats=1, pool=2)
+    assert len(rep.rows) == 2 * len(VARIANTS) * 2
+    for r in rep.rows:
+        assert r["total_us"] > 0 and 0 < r["efficiency"] < 1.5
+        assert r["closed_form_us"] > 0 and len(r["samples_us"]) == 1
+    assert rep.to_csv().splitlines()[0] == "variant,n,width,height,total_us,rate_gbps,efficiency"
+
+
 # ---- config 3 at full size --------------------------------------------------------------
 
 def test_c3_scale_gram_and_clusters():
