@@ -336,14 +336,18 @@ def bench_banded(args, width, height, k, members, eps, rank, world, local_rank):
     from paper_2104_14667_b200.dist import band as row_band
     from paper_2104_14667_b200.synth import synth_cells_gpu
 
-    torch.cuda.set_device(local_rank)
-    N.set_device(local_rank)
+    gpu, backend = dist_setup(local_rank, world)
+    torch.cuda.set_device(gpu)
+    N.set_device(gpu)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dev = torch.device("cuda", local_rank)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
+    dev = torch.device("cuda", gpu)
     row0, rows = row_band(height, rank, world)
     # host RAM bounds how many rows of every mask this rank can hold pinned
     try:
@@ -382,7 +386,7 @@ def bench_banded(args, width, height, k, members, eps, rank, world, local_rank):
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with Clocks(local_rank) as clk:
+    with Clocks(gpu) as clk:
         ev0.record()
         for _ in range(args.steps):
             last = step()
@@ -445,6 +449,17 @@ def bench_banded(args, width, height, k, members, eps, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def dist_setup(local_rank: int, world: int):
+    """(torch device index, backend) for this rank: one GPU per rank over NCCL.  The
+    FS_DIST_BACKEND=gloo override lets a multi-rank run share one GPU (the N > 1 code
+    path exercised on a single-GPU box; not a measurement configuration)."""
+    import torch
+
+    backend = os.environ.get("FS_DIST_BACKEND", "nccl")
+    dev = local_rank % max(1, torch.cuda.device_count()) if backend != "nccl" else local_rank
+    return dev, backend
+
+
 def main():
     args = parse()
     width, height, k, members, eps = CONFIGS[args.config]
@@ -465,14 +480,18 @@ def main():
     from paper_2104_14667_b200.dist import ShardedEnsemble
     from paper_2104_14667_b200.synth import synth_cells, synth_cells_gpu
 
-    torch.cuda.set_device(local_rank)
-    N.set_device(local_rank)
+    gpu, backend = dist_setup(local_rank, world)
+    torch.cuda.set_device(gpu)
+    N.set_device(gpu)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dev = torch.device("cuda", local_rank)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
+    dev = torch.device("cuda", gpu)
     band_h = height
     height = height * world  # weak scaling: every rank keeps a full 1-GPU band
     P = width * height
@@ -516,7 +535,7 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     host_ms = []
-    with Clocks(local_rank) as clk:
+    with Clocks(gpu) as clk:
         barrier()
         ev0.record(stream)
         t_wall0 = time.perf_counter()

@@ -151,10 +151,18 @@ class ShardedEnsemble:
                 b["h_counts"].copy_(b["counts"], non_blocking=True)
                 b["h_rgba"].copy_(b["rgba"], non_blocking=True)
                 b["event_maps"].record(self.d2h_stream)
-        with torch.cuda.stream(self.stream):
+        # the exchange and the small D2H of the partials run on a side stream, so the
+        # next frame's recompute starts right behind this one's kernels (a slot's
+        # buffers are reused only after _finish saw its event)
+        if getattr(self, "x_stream", None) is None:
+            self.x_stream = torch.cuda.Stream(device=self.device)
+        done = torch.cuda.Event()
+        done.record(self.stream)
+        self.x_stream.wait_event(done)
+        with torch.cuda.stream(self.x_stream):
             allreduce_partials(part, self.group)
             b["h_part"].copy_(part, non_blocking=True)
-            b["event"].record(self.stream)
+            b["event"].record(self.x_stream)
 
     def _finish(self, b, ids, tau: float, analytics: bool, maps_to_host: bool, free=None):
         """Wait for a frame's D2H, copy out its histogram and Gram, run the host
