@@ -29,6 +29,7 @@
 //    kernel sums partials into the exact int64 Gram.  Partials are exact: a CTA's K
 //    range is far below 2^31 pixels.
 #include <cstdio>
+#include <cstdlib>
 
 #include "fs_bitslice.cuh"
 
@@ -41,6 +42,7 @@ namespace tc {
 constexpr int kFuseBins = 288;      // SMEM histogram / RGBA table (k <= 256 -> <= 257 bins)
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kRawDepth = 2;
+constexpr int kDefaultFuseDepth = 4;
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
   uint64_t d = 0;
@@ -178,12 +180,12 @@ constexpr uint32_t kSfCol = 448;          // FP4: scale-factor columns [448, 480
 constexpr uint32_t kSfOnes = 0x7F7F7F7Fu; // UE8M0 127 = 2^0 in every byte
 constexpr uint64_t kF4MaxChunkPx = 1ull << 24;  // f32 sums stay exact below this
 
-template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false>
+template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false, int FD = 4>
 struct Cfg {
   // raw ring depth.  FUSE: 4 = one slot per counter warp (unit u lives in slot u % 4 and
   // is counted by warp u % 4), so a counter warp only ever waits on its own slot, in
   // order, and can never run a full mbarrier phase ahead of it.
-  static constexpr int kDepth = FUSE ? 4 : kRawDepth;
+  static constexpr int kDepth = FUSE ? FD : kRawDepth;
   static constexpr int kExtraBytes = FUSE ? (4 * 32 * kTileTb * 4 + 2 * kFuseBins * 4) : 0;
   static constexpr int kBudget = FUSE ? (232448 - 1024 - 256) : kSmemBudget;
   static constexpr int kRegions = DIAG ? 1 : 2;
@@ -208,18 +210,20 @@ struct Cfg {
   static constexpr uint32_t kTmemCols = (PANEL == 256 || FP4) ? 512u : 128u;
   static_assert(!FP4 || DIAG, "FP4 path is for diagonal tiles (off-diagonal accumulators fill TMEM)");
   static_assert(!FUSE || DIAG, "the fused overlap pass runs in diagonal tiles");
-  static_assert(!FUSE || kDepth == 4, "counter warp w owns raw slot w");
+  // FUSE: counter warp u % 4 takes unit u from slot u % kDepth; a slot is refilled
+  // only after that warp released it, so a warp never sees a slot two phases ahead
+  static_assert(!FUSE || kDepth >= 2, "fused pass needs >= 2 raw slots");
   static constexpr int kSmemBytes = kDepth * kRawUnitBytes + kStages * kStageBytes + kExtraBytes +
                                     1024 /*align*/ + 256 /*barriers*/;
   static_assert(kStages >= 2, "operand ring too shallow");
 };
 
-template <int PANEL, bool DIAG, bool FP4, bool FUSE>
-__global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE>::kThreadsTotal, 1)
+template <int PANEL, bool DIAG, bool FP4, bool FUSE, int FD>
+__global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal, 1)
     k_gram_tc(const __grid_constant__ CUtensorMap tm, uint32_t npanels, uint32_t kchunks,
               uint64_t units_per_chunk, uint64_t total_units, int32_t *__restrict__ partial,
               const OverlapArgs ov) {
-  using C = Cfg<PANEL, DIAG, FP4, FUSE>;
+  using C = Cfg<PANEL, DIAG, FP4, FUSE, FD>;
   constexpr int kRawDepth = C::kDepth;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
@@ -847,10 +851,21 @@ size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms, bool fp4) 
   return (size_t)(((uint64_t)p.ndiag * p.kc_diag + (uint64_t)p.noff * p.kc_off) * per_tile);
 }
 
-template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false>
+// raw-ring depth of the fused FP4 kernel (FS_FUSE_DEPTH = 2 | 3 | 4; fewer raw slots
+// leave room for more operand stages)
+static int fuse_depth() {
+  static int d = [] {
+    const char *v = std::getenv("FS_FUSE_DEPTH");
+    const int x = v ? std::atoi(v) : 0;
+    return (x >= 2 && x <= 4) ? x : tc::kDefaultFuseDepth;
+  }();
+  return d;
+}
+
+template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false, int FD = 4>
 static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t *part,
                               const OverlapArgs &ov, cudaStream_t s) {
-  using C = tc::Cfg<PANEL, DIAG, FP4, FUSE>;
+  using C = tc::Cfg<PANEL, DIAG, FP4, FUSE, FD>;
   const uint32_t ntiles = DIAG ? p.ndiag : p.noff;
   const uint32_t kc = DIAG ? p.kc_diag : p.kc_off;
   const uint64_t upc = DIAG ? p.upc_diag : p.upc_off;
@@ -858,13 +873,13 @@ static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t 
   if (ntiles == 0 || kc == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<PANEL, DIAG, FP4, FUSE>,
+    cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<PANEL, DIAG, FP4, FUSE, FD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  tc::k_gram_tc<PANEL, DIAG, FP4, FUSE>
+  tc::k_gram_tc<PANEL, DIAG, FP4, FUSE, FD>
       <<<ntiles * kc, C::kThreadsTotal, C::kSmemBytes, s>>>(
           tm, p.npanels, kc, upc, units, part, ov);
   return cudaGetLastError();
@@ -929,8 +944,10 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
     if ((e = launch_one<128, false>(tm_off, p, part_off, none, s)) != cudaSuccess) return e;
   } else {
     if (fuse_now)
-      e = fp4 ? launch_one<256, true, true, true>(tm_diag, p, part_diag, *fuse, s)
-              : launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s);
+      e = !fp4 ? launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s)
+          : fuse_depth() == 2 ? launch_one<256, true, true, true, 2>(tm_diag, p, part_diag, *fuse, s)
+          : fuse_depth() == 3 ? launch_one<256, true, true, true, 3>(tm_diag, p, part_diag, *fuse, s)
+                              : launch_one<256, true, true, true, 4>(tm_diag, p, part_diag, *fuse, s);
     else
       e = fp4 ? launch_one<256, true, true>(tm_diag, p, part_diag, none, s)
               : launch_one<256, true>(tm_diag, p, part_diag, none, s);
