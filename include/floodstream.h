@@ -157,7 +157,8 @@ int fs_ensemble_set_stream(fs_ensemble *ens, void *stream);
 int fs_ensemble_sync(fs_ensemble *ens);
 /* Choose the Gram engine used by FS_GRAM_AUTO (process-wide). */
 int fs_set_gram_engine(int engine);
-/* Choose the transform kernel: 0 = TMA bulk-staged, 1 = direct vector loads. */
+/* Choose the transform kernel: 0 = TMA bulk-staged, 1 = direct vector loads,
+ * 2 = 8 coalesced 16-B loads in flight per thread (4 KB per warp). */
 int fs_set_pack_engine(int engine);
 
 /* ---- pinned host memory (for zero-staging uploads and fast read-back) ---- */
@@ -182,7 +183,7 @@ int fs_similarity_from_gram(const int64_t *gram, uint32_t n, double *sim);
  * fs_time_transform: mean / min µs (CUDA events, `reps` back-to-back launches) of the
  * binarize + bit-pack transform of one width x height raster already in HBM (iid
  * p = 0.5 depths) — replaces transform_time (device.py:384-390) in the sweep of
- * bench.py:312-339.  engine -1 = current default, 0 = TMA bulk, 1 = direct.
+ * bench.py:312-339.  engine -1 = current default, 0 = TMA bulk, 1 = direct, 2 = vector.
  * fs_time_h2d: one host->device copy of `bytes` from pinned (or pageable) memory —
  * replaces transfer_time (device.py:376-382) in the transfer suite (bench.py:193-228). */
 int fs_time_transform(uint32_t width, uint32_t height, int reps, int engine, double *us_mean,

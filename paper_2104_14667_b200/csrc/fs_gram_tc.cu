@@ -42,7 +42,6 @@ namespace tc {
 constexpr int kFuseBins = 288;      // SMEM histogram / RGBA table (k <= 256 -> <= 257 bins)
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kRawDepth = 2;
-constexpr int kDefaultFuseDepth = 4;
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
   uint64_t d = 0;
@@ -210,9 +209,13 @@ struct Cfg {
   static constexpr uint32_t kTmemCols = (PANEL == 256 || FP4) ? 512u : 128u;
   static_assert(!FP4 || DIAG, "FP4 path is for diagonal tiles (off-diagonal accumulators fill TMEM)");
   static_assert(!FUSE || DIAG, "the fused overlap pass runs in diagonal tiles");
-  // FUSE: counter warp u % 4 takes unit u from slot u % kDepth; a slot is refilled
-  // only after that warp released it, so a warp never sees a slot two phases ahead
-  static_assert(!FUSE || kDepth >= 2, "fused pass needs >= 2 raw slots");
+  // FUSE: counter warp u % 4 takes unit u from slot u % kDepth.  With kDepth a
+  // multiple of 4 the previous occupant of that slot (unit u - kDepth) was counted by
+  // the same warp, so when the warp waits for unit u the slot holds u - kDepth or u and
+  // the phase parity tells them apart.  With fewer slots the previous occupant belongs
+  // to another warp, the expanders may still hold the slot two phases back, and the
+  // parity wait would pass on stale data (caught by the parity tests at depth 2 and 3).
+  static_assert(!FUSE || kDepth % 4 == 0, "counter warp u % 4 must own slot u % kDepth");
   static constexpr int kSmemBytes = kDepth * kRawUnitBytes + kStages * kStageBytes + kExtraBytes +
                                     1024 /*align*/ + 256 /*barriers*/;
   static_assert(kStages >= 2, "operand ring too shallow");
@@ -851,17 +854,6 @@ size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms, bool fp4) 
   return (size_t)(((uint64_t)p.ndiag * p.kc_diag + (uint64_t)p.noff * p.kc_off) * per_tile);
 }
 
-// raw-ring depth of the fused FP4 kernel (FS_FUSE_DEPTH = 2 | 3 | 4; fewer raw slots
-// leave room for more operand stages)
-static int fuse_depth() {
-  static int d = [] {
-    const char *v = std::getenv("FS_FUSE_DEPTH");
-    const int x = v ? std::atoi(v) : 0;
-    return (x >= 2 && x <= 4) ? x : tc::kDefaultFuseDepth;
-  }();
-  return d;
-}
-
 template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false, int FD = 4>
 static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t *part,
                               const OverlapArgs &ov, cudaStream_t s) {
@@ -944,10 +936,8 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
     if ((e = launch_one<128, false>(tm_off, p, part_off, none, s)) != cudaSuccess) return e;
   } else {
     if (fuse_now)
-      e = !fp4 ? launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s)
-          : fuse_depth() == 2 ? launch_one<256, true, true, true, 2>(tm_diag, p, part_diag, *fuse, s)
-          : fuse_depth() == 3 ? launch_one<256, true, true, true, 3>(tm_diag, p, part_diag, *fuse, s)
-                              : launch_one<256, true, true, true, 4>(tm_diag, p, part_diag, *fuse, s);
+      e = fp4 ? launch_one<256, true, true, true>(tm_diag, p, part_diag, *fuse, s)
+              : launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s);
     else
       e = fp4 ? launch_one<256, true, true>(tm_diag, p, part_diag, none, s)
               : launch_one<256, true>(tm_diag, p, part_diag, none, s);

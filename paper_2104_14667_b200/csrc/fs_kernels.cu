@@ -115,6 +115,31 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Vector variant: a warp turns one 4 KB block into 128 words; every thread keeps 8
+// coalesced 16-B loads in flight (lane t, load i: bytes 512 i + 16 t), lane pairs merge
+// their 16-px nibble sets into one 32-px word.
+constexpr int kPackVec = 8;
+constexpr int kPackBlk = kPackVec * 512;  // bytes (pixels) per warp-block
+__global__ void __launch_bounds__(256)
+    k_pack_vec(const uint8_t *__restrict__ src, uint64_t nblk, uint32_t *__restrict__ dst,
+               uint64_t slot, uint64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nblk; b += nw) {
+    const uint8_t *base = src + b * kPackBlk + lane * 16;
+    uint4 v[kPackVec];
+#pragma unroll
+    for (int i = 0; i < kPackVec; ++i) v[i] = ptx::ld_nc_v4(base + i * 512);
+#pragma unroll
+    for (int i = 0; i < kPackVec; ++i) {
+      const uint32_t h = nz_bits16(v[i]);
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
+      if ((lane & 1) == 0)
+        dst[pk_off(slot, b * (kPackBlk / 32) + i * 16 + (lane >> 1), cap)] = h | (other << 16);
+    }
+  }
+}
+
 // Words [w0, wpm): scalar tail + zero padding.
 __global__ void k_pack_tail(const uint8_t *__restrict__ src, uint64_t pixels, uint64_t w0,
                             uint64_t wpm, uint32_t *__restrict__ dst, uint64_t slot,
@@ -149,6 +174,15 @@ cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint
       if (grid > nchunks) grid = nchunks;
       k_pack_bulk<<<(unsigned)grid, kPackThreads, smem, s>>>(src, nchunks, dst, slot, cap);
       done_words = nchunks * (kPackChunk / 32);
+    }
+  } else if (engine == 2) {
+    const uint64_t nblk = pixels / kPackBlk;
+    if (nblk > 0) {
+      uint64_t grid = (nblk * 32 + 255) / 256;
+      const uint64_t gcap = (uint64_t)num_sms() * 8;
+      if (grid > gcap) grid = gcap;
+      k_pack_vec<<<(unsigned)grid, 256, 0, s>>>(src, nblk, dst, slot, cap);
+      done_words = nblk * (kPackBlk / 32);
     }
   } else {
     // full 32-byte groups only; the rest goes to the tail kernel

@@ -253,6 +253,9 @@ class ResidentEngine:
             t0 = time.perf_counter()
             moved = self.update(ids, load) if load is not None else None
             ids = list(dict.fromkeys(ids))
+            missing = [s for s in ids if s not in self.slots.slot_of]
+            if missing:
+                raise KeyError(f"surfaces not resident (pass a loader): {missing[:5]}")
             if not ids:
                 return EngineSnapshot(version, [], self.width, self.height, 0,
                                       [self.width * self.height], report={"uploaded": 0})

@@ -201,7 +201,7 @@ def test_gram_large_pixels(engine):
 # ---- transform, synth ------------------------------------------------------------------
 
 @pytest.mark.parametrize("pixels", [1, 31, 8191, 8192, 8193, 3 * 8192 + 17, 1 << 20, 612 * 499])
-@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("engine", [0, 1, 2])
 def test_pack_engines(pixels, engine):
     rng = np.random.default_rng(pixels)
     cells = [rng.integers(0, 3, pixels).astype(np.uint8).reshape(1, pixels) for _ in range(3)]

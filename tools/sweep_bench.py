@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default=None)
     ap.add_argument("--quick", action="store_true", help="8x8 grids (smoke)")
+    ap.add_argument("--engine", type=int, default=-1,
+                    help="transform kernel: -1 default, 0 TMA bulk, 1 direct, 2 vector")
     args = ap.parse_args()
 
     from paper_2104_14667_b200 import _native as N
@@ -48,13 +50,15 @@ def main():
     if args.quick:
         specs = {"nonpow2": SweepSpec(512, 2000, 16012), "pow2": SweepSpec(512, 2048, 16384)}
     doc = {"config": "c5: raster dimension sweep 512-16384 (non-square, non-pow2), iid p=0.5",
-           "kernel": "k_pack_bulk (TMA bulk-staged binarize + bit-pack)",
+           "kernel": {-1: "library default", 0: "k_pack_bulk (TMA bulk-staged)",
+                      1: "k_pack_direct", 2: "k_pack_vec (8 x 16-B loads in flight)"}[args.engine]
+                     + " binarize + bit-pack",
            "rate_def": "w*h / t_us / 1000 GB/s of uint8 raster (fs/bench.py:337-338)",
            "roofline": {"bound": "hbm", "bytes_per_px": 1.125, "peak_gbs": hbm,
                         "raster_rate_ceiling_gbs": round(hbm / 1.125, 1)}}
     for name, spec in specs.items():
         t0 = time.perf_counter()
-        rm = run_transform_sweep(spec, reps=args.reps)
+        rm = run_transform_sweep(spec, reps=args.reps, engine=args.engine)
         r = rm.rates
         big = r[len(spec.points) // 2:, len(spec.points) // 2:]
         doc[name] = {"ratemap": rm.to_json(), "seconds": round(time.perf_counter() - t0, 2),
