@@ -179,6 +179,15 @@ int fs_outlier_scores(const double *sim, uint32_t n, double *scores);
 /* sim[i,j] = inter/union (1.0 when union == 0), diag 1.0, from an int64 Gram.      */
 int fs_similarity_from_gram(const int64_t *gram, uint32_t n, double *sim);
 
+/* The same two products on the device, for the resident recompute: `gram` (n x n
+ * int64), `sim` (n x n float64) and `scores` (n float64, may be NULL) are DEVICE
+ * pointers; the kernels are queued on `stream` (a cudaStream_t; NULL = the calling
+ * thread's stream) and the call returns without waiting.  Bit-identical to
+ * fs_similarity_from_gram / fs_outlier_scores (IEEE division, one left-to-right sum
+ * per row).                                                                        */
+int fs_similarity_outliers_device(const int64_t *gram, uint32_t n, double *sim, double *scores,
+                                  void *stream);
+
 /* ---- measured timings: the reference's modelled costs, on the device -----------
  * fs_time_transform: mean / min µs (CUDA events, `reps` back-to-back launches) of the
  * binarize + bit-pack transform of one width x height raster already in HBM (iid

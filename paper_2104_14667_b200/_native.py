@@ -87,6 +87,7 @@ _SIGNATURES = {
     "fs_cluster_complete_linkage": [_f64p, C.c_uint32, _u32p, C.c_double, _i32p],
     "fs_outlier_scores": [_f64p, C.c_uint32, _f64p],
     "fs_similarity_from_gram": [_i64p, C.c_uint32, _f64p],
+    "fs_similarity_outliers_device": [_vp, C.c_uint32, _vp, _vp, _vp],
     "fs_time_transform": [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.POINTER(C.c_double),
                           C.POINTER(C.c_double)],
     "fs_time_h2d": [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)],

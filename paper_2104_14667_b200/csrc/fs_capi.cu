@@ -1061,6 +1061,21 @@ int fs_similarity_from_gram(const int64_t *gram, uint32_t n, double *sim) {
   return FS_OK;
 }
 
+int fs_similarity_outliers_device(const int64_t *gram, uint32_t n, double *sim, double *scores,
+                                  void *stream) {
+  if (!gram || !sim) return set_err(FS_EINVAL, "null buffer");
+  if (scores && n < 2) return set_err(FS_EINVAL, "outlier scores need at least two surfaces");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!s) {
+    ThreadCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    s = c->s;
+  }
+  CK(launch_similarity_outliers(reinterpret_cast<const long long *>(gram), n, sim, scores, s));
+  return FS_OK;
+}
+
 int fs_outlier_scores(const double *sim, uint32_t n, double *scores) {
   if (!sim || !scores) return set_err(FS_EINVAL, "null buffer");
   if (n < 2) return set_err(FS_EINVAL, "outlier scores need at least two surfaces");

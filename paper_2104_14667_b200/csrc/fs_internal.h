@@ -94,6 +94,9 @@ cudaError_t launch_synth_packed(uint32_t *packed, uint64_t slot, uint64_t capaci
 cudaError_t launch_synth_raw(uint8_t *dst, const SynthParams &sp, uint64_t mask, uint64_t row0,
                              uint64_t pixels, cudaStream_t s);
 
+cudaError_t launch_similarity_outliers(const long long *gram, uint32_t n, double *sim,
+                                       double *scores, cudaStream_t s);
+
 // Composite grey LUT in FP64, bit-exact with _kernels_np.py:41-42.
 void build_grey_lut(uint64_t n_inputs, uint8_t *lut, uint64_t entries);
 uint8_t grey_of(uint64_t c, uint64_t n_inputs);

@@ -53,7 +53,7 @@ __device__ __forceinline__ uint32_t nz_bits16(uint4 v) {
 constexpr int kPackThreads = 256;
 constexpr int kPackChunk = 8192;  // bytes (= pixels) per stage, 256 output words
 constexpr int kPackStages = 4;
-static int g_pack_engine = 0;
+static int g_pack_engine = 2;  // k_pack_vec: measured fastest (profiles/r1x)
 void set_pack_engine(int e) { g_pack_engine = e; }
 int get_pack_engine() { return g_pack_engine; }
 
@@ -789,6 +789,51 @@ cudaError_t launch_synth_raw(uint8_t *dst, const SynthParams &sp, uint64_t mask,
   const uint64_t cap = (uint64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
   k_synth_raw<<<(unsigned)grid, 256, 0, s>>>(dst, sp, mask, row0, pixels);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Jaccard matrix + outlier scores from the exact int64 Gram, on the device
+// (analytics.py:165-181 and :229-240 of the reference).  Jaccard = inter / union in
+// IEEE double (exact integer operands below 2^53, correctly rounded division = Python's
+// int/int true division), 1.0 on the diagonal and for empty unions.  Outlier score of
+// row i = 1 - (left-to-right double sum over j != i) / (n - 1): one thread per row keeps
+// the reference's summation order, so the result is bit-identical to the host's.
+// ---------------------------------------------------------------------------
+__global__ void k_similarity(const long long *__restrict__ gram, uint32_t n, double *__restrict__ sim) {
+  const uint64_t total = (uint64_t)n * n;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(e / n), j = (uint32_t)(e % n);
+    double v = 1.0;
+    if (i != j) {
+      const long long inter = gram[e];
+      const long long uni = gram[(uint64_t)i * n + i] + gram[(uint64_t)j * n + j] - inter;
+      if (uni != 0) v = __ddiv_rn((double)inter, (double)uni);
+    }
+    sim[e] = v;
+  }
+}
+
+__global__ void k_outliers(const double *__restrict__ sim, uint32_t n, double *__restrict__ scores) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double *r = sim + (uint64_t)i * n;
+  double acc = 0.0;
+  for (uint32_t j = 0; j < n; ++j)
+    if (j != i) acc = __dadd_rn(acc, r[j]);
+  scores[i] = __dsub_rn(1.0, __ddiv_rn(acc, (double)(n - 1)));
+}
+
+cudaError_t launch_similarity_outliers(const long long *gram, uint32_t n, double *sim,
+                                       double *scores, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint64_t total = (uint64_t)n * n;
+  uint64_t grid = (total + 255) / 256;
+  const uint64_t gcap = (uint64_t)num_sms() * 8;
+  if (grid > gcap) grid = gcap;
+  k_similarity<<<(unsigned)grid, 256, 0, s>>>(gram, n, sim);
+  if (scores != nullptr && n >= 2) k_outliers<<<(n + 127) / 128, 128, 0, s>>>(sim, n, scores);
   return cudaGetLastError();
 }
 

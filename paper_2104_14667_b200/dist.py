@@ -21,6 +21,8 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _native as N
+
 
 def band(height: int, rank: int, world: int) -> tuple[int, int]:
     """(row0, rows) of rank's band: rows split as evenly as possible, lower ranks first."""
@@ -113,6 +115,12 @@ class ShardedEnsemble:
                  counts=torch.empty(px, dtype=torch.int32, device=self.device),
                  rgba=torch.empty(px * 4, dtype=torch.uint8, device=self.device),
                  h_part=torch.empty(total, dtype=torch.int64).pin_memory(),
+                 # Jaccard matrix + outlier scores, computed on the device from the
+                 # summed Gram (fs_similarity_outliers_device)
+                 sim=torch.empty(k * k, dtype=torch.float64, device=self.device),
+                 scores=torch.empty(max(k, 1), dtype=torch.float64, device=self.device),
+                 h_sim=torch.empty(k * k, dtype=torch.float64).pin_memory(),
+                 h_scores=torch.empty(max(k, 1), dtype=torch.float64).pin_memory(),
                  event=torch.cuda.Event())
         if maps:
             b["h_counts"] = torch.empty(px, dtype=torch.int32).pin_memory()
@@ -161,7 +169,13 @@ class ShardedEnsemble:
         self.x_stream.wait_event(done)
         with torch.cuda.stream(self.x_stream):
             allreduce_partials(part, self.group)
+            k = b["k"]
+            N.call("fs_similarity_outliers_device", part.data_ptr() + b["nb"] * 8, k,
+                   b["sim"].data_ptr(), b["scores"].data_ptr() if k >= 2 else None,
+                   self.x_stream.cuda_stream)
             b["h_part"].copy_(part, non_blocking=True)
+            b["h_sim"].copy_(b["sim"], non_blocking=True)
+            b["h_scores"].copy_(b["scores"], non_blocking=True)
             b["event"].record(self.x_stream)
 
     def _finish(self, b, ids, tau: float, analytics: bool, maps_to_host: bool, free=None):
@@ -169,7 +183,7 @@ class ShardedEnsemble:
         analytics; then hand the buffer slot back (``free``).  Runs on a pool thread:
         the C analytics release the GIL, so frames' host work overlaps each other and
         the main thread's enqueueing."""
-        from .analytics import cluster_from_similarity, outliers_from_similarity, similarity_from_gram
+        from .analytics import cluster_from_similarity
 
         try:
             b["event"].synchronize()
@@ -187,9 +201,13 @@ class ShardedEnsemble:
                     free.set()
                     free = None
             if analytics:
-                sim = similarity_from_gram(out["gram"])
+                sim = b["h_sim"].numpy().reshape(k, k).copy()
                 out["similarity"] = sim
-                out["outliers"] = outliers_from_similarity(sim, ids) if len(ids) >= 2 else None
+                if k >= 2:
+                    sc = b["h_scores"].numpy()
+                    out["outliers"] = {sid: sc[i] for i, sid in enumerate(ids)}
+                else:
+                    out["outliers"] = None
                 out["clusters"] = cluster_from_similarity(sim, ids, tau)
             return out
         finally:

@@ -212,7 +212,7 @@ def test_pack_engines(pixels, engine):
             c, b, r = ens.overlap([0, 1, 2])
             g = ens.gram([0, 1, 2], engine="popc")
     finally:
-        N.call("fs_set_pack_engine", 0)
+        N.call("fs_set_pack_engine", 2)
     want = O.accumulate(cells, pixels, 1)
     assert np.array_equal(c, want)
     assert np.array_equal(g, O.gram(cells))
@@ -462,3 +462,30 @@ def test_gram_pair_kernel_multi_panel(k, h, w):
     assert np.array_equal(got, ref)
     if h * w <= 100_000:
         assert np.array_equal(got, O.gram(cells))
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 64, 300])
+def test_device_similarity_and_outliers_bitwise(k):
+    """fs_similarity_outliers_device (the frame pipeline's Jaccard + outliers) equals the
+    reference formulas bit for bit, empty unions included."""
+    import torch
+
+    rng = np.random.default_rng(k)
+    cells = [(rng.random(500) < rng.uniform(0.05, 0.95)).astype(np.uint8) for _ in range(k)]
+    if k > 2:
+        cells[1] = np.zeros(500, np.uint8)
+        cells[2] = np.zeros(500, np.uint8)
+    g = O.gram(cells)
+    d_g = torch.from_numpy(g).cuda()
+    d_s = torch.empty(k * k, dtype=torch.float64, device="cuda")
+    d_o = torch.empty(max(k, 1), dtype=torch.float64, device="cuda")
+    N.call("fs_similarity_outliers_device", d_g.data_ptr(), k, d_s.data_ptr(),
+           d_o.data_ptr() if k >= 2 else None, None)
+    N.call("fs_synchronize")
+    sim = O.similarity_from_gram(g)
+    assert d_s.cpu().numpy().reshape(k, k).tobytes() == sim.tobytes()
+    if k >= 2:
+        ids = [f"s{i}" for i in range(k)]
+        want = O.outlier_scores(sim, ids)
+        got = d_o.cpu().numpy()
+        assert [float(x).hex() for x in got] == [float(want[i]).hex() for i in ids]
