@@ -620,16 +620,16 @@ def main():
     if fused and args.engine == "tc-f4" and k > 128:
         # What actually limits the fused kernel: shared-memory bandwidth (128 B/clk/SM).
         # Per 256-px K stage of the 256-mask diagonal panel the MMAs read 80 KB of
-        # operands (rows 0-127 x N=256 and rows 128-255 x N=128, 4 K-steps), the
-        # expanders write 32 KB of e2m1 operands and read 8 KB of raw bits, and the
-        # counter warps read the same 8 KB; the MMAs alone need 768 cycles.
+        # operands (rows 0-127 x N=256 and rows 128-255 x N=128, 4 K-steps), TMA writes
+        # 8 KB of raw bits, the expanders read them and write 32 KB of e2m1 operands,
+        # and the counter warps read the same 8 KB; the MMAs alone need 768 cycles.
         clk_hz = float((clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         stages = -(-P_band // 1024) * 4 / nsm
-        smem_ms = stages * (128 * 1024 / 128) / clk_hz * 1e3
+        smem_ms = stages * (136 * 1024 / 128) / clk_hz * 1e3
         mma_ms = stages * 768 / clk_hz * 1e3
         rl_fused["limiter_model"] = {
-            "limiter": "smem", "smem_bytes_per_stage": 128 * 1024, "smem_bytes_per_clk": 128,
+            "limiter": "smem", "smem_bytes_per_stage": 136 * 1024, "smem_bytes_per_clk": 128,
             "mma_cycles_per_stage": 768, "stages_per_sm": round(stages, 1),
             "smem_bound_ms": round(smem_ms, 4), "mma_bound_ms": round(mma_ms, 4),
             "frac_of_smem_bound": round(smem_ms / rc_ms, 4),
@@ -720,7 +720,9 @@ def main():
         else:
             gram_launches = 1 + (1 if k > 64 else 0)  # popc, mirror
         # + the overlap kernel unless fused into the diagonal Gram CTAs
-        line["gpu_launches"] = (gram_launches + (0 if fused else 1)) * args.steps
+        # + Jaccard and outlier kernels on the summed Gram
+        analytic_launches = 2 if k >= 2 else 1
+        line["gpu_launches"] = (gram_launches + (0 if fused else 1) + analytic_launches) * args.steps
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
     sh.close()
