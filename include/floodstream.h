@@ -23,6 +23,12 @@
  *                          service.py:143-175 (resident recompute of the working set)
  *   fs_cluster_complete_linkage <- analytics.py:184-226 cluster_surfaces() merge loop
  *   fs_outlier_scores   <- analytics.py:229-240   outlier_scores() reduction
+ *   fs_similarity_from_gram, fs_similarity_outliers_device
+ *                       <- analytics.py:165-181   jaccard() / similarity_matrix() on the
+ *                          exact pair counts, and :229-240 (on the device)
+ *   fs_time_transform / fs_time_h2d <- device.py:376-401 transform_time / transfer_time
+ *                          (the reference's modelled costs, measured)
+ *   fs_synth_host / fs_synth_gpu    <- bench.py:472-475 input generation (test/bench input)
  */
 #ifndef FLOODSTREAM_H
 #define FLOODSTREAM_H
