@@ -3,9 +3,10 @@
 
 Workload (BASELINE.json configs[1], "c2"): 256 flood-like masks of 8192 x 8192 uint8
 (17.18 GB).  One *step* = one full recompute of the working set:
-  overlap counts + overlap-class histogram + composite RGBA (one fused pass over the
-  bit-packed masks), the exact pairwise-intersection Gram (tcgen05 int8), and on the
-  host the Jaccard matrix, outlier scores and complete-linkage clusters (tau 0.8).
+  overlap counts + overlap-class histogram + composite RGBA and the exact
+  pairwise-intersection Gram in ONE kernel over the bit-packed masks (tcgen05
+  kind::mxf4 + counter warps), the Jaccard matrix and outlier scores on the device, and
+  the complete-linkage clusters (tau 0.8) on the host.
 
 * ``value``: masks already resident (bit-packed) in HBM; unit Gpx/s = N*P / step time.
 * ``e2e``  : the same step through the public API from PINNED host rasters: every step
