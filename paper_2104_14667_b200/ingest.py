@@ -13,6 +13,7 @@ the device) — the paper's host[i] -> copy[i] -> transform[i] overlap, from fil
 from __future__ import annotations
 
 import os
+import threading
 from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
@@ -81,6 +82,31 @@ def decode_into(source, out: np.ndarray) -> tuple[int, int]:
     return w, h
 
 
+_pool_lock = threading.Lock()
+_pool: dict = {}  # (pixels, batch) -> two halves of pinned buffers, reused across calls
+
+
+def _staging(P: int, batch: int):
+    """Two batches of pinned staging buffers (page-locking 2 x batch x P bytes costs
+    far more than a read, so they are kept for the next call of the same shape)."""
+    with _pool_lock:
+        bufs = _pool.pop((P, batch), None)
+    return bufs or [[N.PinnedBuffer((P,)) for _ in range(batch)] for _ in range(2)]
+
+
+def _release(P: int, batch: int, bufs) -> None:
+    """Keep ``bufs`` for the next call; free whatever the pool held before (at most one
+    shape stays page-locked)."""
+    with _pool_lock:
+        stale = list(_pool.values())
+        _pool.clear()
+        _pool[(P, batch)] = bufs
+    for halves in stale:
+        for half in halves:
+            for buf in half:
+                buf.free()
+
+
 def stream_files(ens, sources, *, first: int = 0, batch: int = 16, workers: int | None = None,
                  ids=None) -> dict:
     """Decode ``sources`` (paths or bytes) into two pinned batches of ``batch`` buffers
@@ -93,7 +119,7 @@ def stream_files(ens, sources, *, first: int = 0, batch: int = 16, workers: int 
         raise ValueError("sources exceed the ensemble's capacity")
     P = ens.pixels
     batch = max(1, min(batch, n))
-    bufs = [[N.PinnedBuffer((P,)) for _ in range(batch)] for _ in range(2)]
+    bufs = _staging(P, batch)
     workers = workers or min(16, (os.cpu_count() or 4))
     t0 = time.perf_counter()
     upload_us = 0.0
@@ -116,9 +142,7 @@ def stream_files(ens, sources, *, first: int = 0, batch: int = 16, workers: int 
                                 ids=None if ids is None else ids[lo:lo + len(cur)])
                 upload_us += st.total_us
     finally:
-        for half in bufs:
-            for buf in half:
-                buf.free()
+        _release(P, batch, bufs)
     wall = time.perf_counter() - t0
     return {"files": n, "bytes": n * P, "wall_s": wall, "upload_s": upload_us / 1e6,
             "rate_gbs": n * P / wall / 1e9 if wall > 0 else None}
