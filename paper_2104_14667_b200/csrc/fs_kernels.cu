@@ -815,13 +815,15 @@ __global__ void k_similarity(const long long *__restrict__ gram, uint32_t n, dou
   }
 }
 
+// Row i's sum walks column i instead (sim is exactly symmetric: the Gram is mirrored
+// and inter / (g_ii + g_jj - inter) is the same double either way), so at step j the
+// threads of a warp read consecutive addresses.
 __global__ void k_outliers(const double *__restrict__ sim, uint32_t n, double *__restrict__ scores) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double *r = sim + (uint64_t)i * n;
   double acc = 0.0;
   for (uint32_t j = 0; j < n; ++j)
-    if (j != i) acc = __dadd_rn(acc, r[j]);
+    if (j != i) acc = __dadd_rn(acc, sim[(uint64_t)j * n + i]);
   scores[i] = __dsub_rn(1.0, __ddiv_rn(acc, (double)(n - 1)));
 }
 
@@ -833,7 +835,7 @@ cudaError_t launch_similarity_outliers(const long long *gram, uint32_t n, double
   const uint64_t gcap = (uint64_t)num_sms() * 8;
   if (grid > gcap) grid = gcap;
   k_similarity<<<(unsigned)grid, 256, 0, s>>>(gram, n, sim);
-  if (scores != nullptr && n >= 2) k_outliers<<<(n + 127) / 128, 128, 0, s>>>(sim, n, scores);
+  if (scores != nullptr && n >= 2) k_outliers<<<(n + 31) / 32, 32, 0, s>>>(sim, n, scores);
   return cudaGetLastError();
 }
 
