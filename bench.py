@@ -606,19 +606,23 @@ def main():
                           "(the kernel issues 3/4 N^2 P MACs: 128-row MMA granularity)",
                "peak_note": t_kind}
     rc_ms = statistics.median(kern["recompute"])
-    rl_fused = {"bound": "tensor", "kernel": "k_gram_tc<...,FUSE> + k_gram_reduce" if fused
+    npanels_k = -(-k // (128 if k <= 128 else 256))
+    rl_fused = {"bound": "tensor",
+                "kernel": ("k_gram_tc<...,FUSE> + k_gram_reduce" if npanels_k == 1 else
+                           "k_gram_tc<...,FUSE> (partial counts) + k_gram_pair_f4 + "
+                           "k_gram_reduce + k_combine_partials") if fused
                 else "k_overlap + k_gram_tc + k_gram_reduce",
                 "fused": bool(fused), "achieved": round(gram_ops / rc_ms / 1e9, 1),
                 "peak": t_peak, "unit": "TFLOP/s",
                 "frac": round(gram_ops / rc_ms / 1e9 / t_peak, 4),
-                "traffic": traffic.get("k_gram_tc_fused") if fused else None,
+                "traffic": traffic.get("k_gram_tc_fused") if (fused and npanels_k == 1) else None,
                 "kernel_ms": round(rc_ms, 4), "ops_per_launch": gram_ops,
                 "ops_def": rl_gram["ops_def"], "peak_note": t_kind,
                 "hbm_achieved_gbs": round(ov_bytes / rc_ms / 1e6, 1),
                 "hbm_frac": round(ov_bytes / rc_ms / 1e6 / hbm, 4),
                 "hbm_bytes_def": "same algorithmic bytes as the overlap pass (the Gram reads "
                                  "the same packed tiles)"}
-    if fused and args.engine == "tc-f4" and k > 128:
+    if fused and args.engine == "tc-f4" and k > 128 and npanels_k == 1:
         # What actually limits the fused kernel: shared-memory bandwidth (128 B/clk/SM).
         # Per 256-px K stage of the 256-mask diagonal panel the MMAs read 80 KB of
         # operands (rows 0-127 x N=256 and rows 128-255 x N=128, 4 K-steps), TMA writes
@@ -720,10 +724,13 @@ def main():
             gram_launches = 1 + (1 if npanels > 1 else 0) + 1  # diag, off-diag, reduce
         else:
             gram_launches = 1 + (1 if k > 64 else 0)  # popc, mirror
-        # + the overlap kernel unless fused into the diagonal Gram CTAs
+        # + the overlap kernel unless fused into the diagonal Gram CTAs (beyond one panel
+        # the fused path adds a combine kernel instead)
         # + Jaccard and outlier kernels on the summed Gram
         analytic_launches = 2 if k >= 2 else 1
-        line["gpu_launches"] = (gram_launches + (0 if fused else 1) + analytic_launches) * args.steps
+        npan = -(-k // (128 if k <= 128 else 256))
+        line["gpu_launches"] = (gram_launches + (0 if (fused and npan == 1) else 1)
+                                + analytic_launches) * args.steps
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
     sh.close()

@@ -162,4 +162,27 @@ __device__ __forceinline__ void emit_tile(const uint32_t (&cnt32)[32], uint64_t 
   __syncwarp();
 }
 
+// Partial counts of one 1024-px tile as uint16 (multi-panel fused recompute): the
+// same SMEM transpose as emit_tile, then lane l writes 8 consecutive pixels (16 B) of
+// word 8 it + l / 4 — a warp stores 512 contiguous bytes per iteration.
+__device__ __forceinline__ void emit_partial16(const uint32_t (&cnt32)[32], uint64_t tile,
+                                               int lane, uint32_t *tb, uint16_t *dst) {
+  uint32_t *row = tb + lane * kTileTb;
+#pragma unroll
+  for (int v = 0; v < 8; ++v)
+    *reinterpret_cast<uint4 *>(row + 4 * v) =
+        make_uint4(cnt32[4 * v], cnt32[4 * v + 1], cnt32[4 * v + 2], cnt32[4 * v + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int w = it * 8 + (lane >> 2), b0 = (lane & 3) * 8;
+    const uint4 c0 = *reinterpret_cast<const uint4 *>(tb + w * kTileTb + b0);
+    const uint4 c1 = *reinterpret_cast<const uint4 *>(tb + w * kTileTb + b0 + 4);
+    const uint4 o = make_uint4(c0.x | (c0.y << 16), c0.z | (c0.w << 16), c1.x | (c1.y << 16),
+                               c1.z | (c1.w << 16));
+    st_cs_v4(dst + tile * 1024 + (uint64_t)w * 32 + b0, o);
+  }
+  __syncwarp();
+}
+
 }  // namespace fs

@@ -776,7 +776,7 @@ int gram_dispatch(fs_ensemble *e, const uint32_t *slots, uint32_t k, int engine,
     return FS_OK;
   }
   const bool fp4 = engine == FS_GRAM_TC_F4;
-  CK(e->ws.ensure(gram_tc_workspace_bytes(k, e->wpm, e->num_sms, fp4)));
+  CK(e->ws.ensure(gram_tc_workspace_bytes(k, e->wpm, e->num_sms, fp4, fuse != nullptr)));
   void *gws = nullptr;
   if (contiguous_run(slots, k) < 0) {
     CK(e->gather.ensure(gram_tc_gather_bytes(k, e->wpm)));

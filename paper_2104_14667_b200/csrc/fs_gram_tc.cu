@@ -402,8 +402,12 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
 #pragma unroll
       for (int j = 0; j < 32; ++j) cnt32[j] = 0;
       hc.extract(cnt32, 1u);
-      emit_tile(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
-                ov.bins != nullptr, sh_lut, lut_sh);
+      if (ov.partial16 != nullptr)  // multi-panel: this panel's counts, summed later
+        emit_partial16(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb,
+                       ov.partial16 + (uint64_t)I * ov.part_pitch);
+      else
+        emit_tile(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
+                  ov.bins != nullptr, sh_lut, lut_sh);
     }
   } else {
     // ===== expanders: raw bits (swizzled) -> 0/1 bytes in SW128 K-major operand =====
@@ -848,10 +852,19 @@ static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms, bool fp4) {
 
 }  // namespace tc
 
-size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms, bool fp4) {
-  tc::Plan p = tc::make_plan(k, wpm, num_sms, fp4);
+static uint64_t partial_offset(const tc::Plan &p) {
   const uint64_t per_tile = (uint64_t)p.panel * p.panel * 4;
-  return (size_t)(((uint64_t)p.ndiag * p.kc_diag + (uint64_t)p.noff * p.kc_off) * per_tile);
+  const uint64_t b = ((uint64_t)p.ndiag * p.kc_diag + (uint64_t)p.noff * p.kc_off) * per_tile;
+  return (b + 255) / 256 * 256;
+}
+
+size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms, bool fp4, bool fuse) {
+  tc::Plan p = tc::make_plan(k, wpm, num_sms, fp4);
+  uint64_t bytes = partial_offset(p);
+  // multi-panel fused recompute: one uint16 partial-count slab per panel
+  if (fuse && fp4 && p.panel == 256 && p.npanels > 1)
+    bytes += (uint64_t)p.npanels * (wpm / 32) * 1024 * 2;
+  return (size_t)bytes;
 }
 
 template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false, int FD = 4>
@@ -925,6 +938,21 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
   // one panel holds every mask: its diagonal CTAs see all masks of a pixel range and
   // also produce the overlap products (counts / histogram / RGBA) from the same tiles
   const bool fuse_now = fuse != nullptr && p.npanels == 1;
+  // several 256-mask panels (FP4): each diagonal CTA counts its panel's masks from the
+  // tiles it already streams (uint16 partial counts); a combine pass sums the panels
+  const bool fuse_multi = fuse != nullptr && p.npanels > 1 && fp4 && p.panel == 256;
+  OverlapArgs ovp{};
+  uint16_t *partial16 = nullptr;
+  const uint64_t pitch = ntiles * 1024;
+  if (fuse_multi) {
+    partial16 = reinterpret_cast<uint16_t *>(static_cast<char *>(workspace) + partial_offset(p));
+    ovp = *fuse;
+    ovp.counts = nullptr;
+    ovp.rgba = nullptr;
+    ovp.bins = nullptr;
+    ovp.partial16 = partial16;
+    ovp.part_pitch = pitch;
+  }
   if (p.panel == 128) {
     if (fuse_now)
       e = fp4 ? launch_one<128, true, true, true>(tm_diag, p, part_diag, *fuse, s)
@@ -938,6 +966,8 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
     if (fuse_now)
       e = fp4 ? launch_one<256, true, true, true>(tm_diag, p, part_diag, *fuse, s)
               : launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s);
+    else if (fuse_multi)
+      e = launch_one<256, true, true, true>(tm_diag, p, part_diag, ovp, s);
     else
       e = fp4 ? launch_one<256, true, true>(tm_diag, p, part_diag, none, s)
               : launch_one<256, true>(tm_diag, p, part_diag, none, s);
@@ -959,7 +989,7 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
       return e;
     }
   }
-  if (fused) *fused = fuse_now;
+  if (fused) *fused = fuse_now || fuse_multi;
   const uint64_t total = (uint64_t)(p.ndiag + p.noff) * per_tile;
   uint64_t grid = (total + 255) / 256;
   if (grid > (uint64_t)num_sms * 8) grid = (uint64_t)num_sms * 8;
@@ -969,7 +999,9 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
   else
     tc::k_gram_reduce<256><<<(unsigned)grid, 256, 0, s>>>(part_diag, p.kc_diag, part_off,
                                                            p.kc_off, k, p.npanels, gram);
-  return cudaGetLastError();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (fuse_multi) return launch_combine_partials(partial16, p.npanels, pitch, *fuse, s);
+  return cudaSuccess;
 }
 
 }  // namespace fs

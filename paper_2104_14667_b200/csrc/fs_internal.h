@@ -61,8 +61,16 @@ struct OverlapArgs {
   uint64_t n_inputs;
   const uint8_t *lut;         // grey LUT of nbins entries, or null (FP64 path)
   int vec;                    // set by launch_overlap: outputs 16-B aligned
+  // Multi-panel fused recompute: the diagonal Gram CTAs of panel I write the counts of
+  // their <= 256 masks as uint16 to partial16 + I * part_pitch (instead of counts /
+  // RGBA / bins); launch_combine_partials then sums the panels into the outputs.
+  uint16_t *partial16 = nullptr;
+  uint64_t part_pitch = 0;    // pixels per panel slab (multiple of 1024)
 };
 cudaError_t launch_overlap(const OverlapArgs &a, cudaStream_t s);
+// counts / RGBA / bins of `a` from npanels uint16 partial-count slabs
+cudaError_t launch_combine_partials(const uint16_t *partial16, uint32_t npanels, uint64_t pitch,
+                                    const OverlapArgs &a, cudaStream_t s);
 
 cudaError_t launch_accumulate_packed(const uint32_t *packed, uint64_t slot, uint64_t capacity,
                                      uint64_t pixels, uint32_t *counts, cudaStream_t s);
@@ -72,7 +80,8 @@ cudaError_t launch_gram_popc(const uint32_t *packed, uint64_t capacity, uint64_t
                              cudaStream_t s);
 // tcgen05 kind::i8 Gram; partial workspace sized by gram_tc_workspace_bytes().
 // fp4: diagonal tiles on kind::mxf4 (off-diagonal tiles stay on kind::i8).
-size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms, bool fp4);
+size_t gram_tc_workspace_bytes(uint32_t k, uint64_t wpm, int num_sms, bool fp4,
+                               bool fuse = false);
 // Non-contiguous slot lists are first gathered into gather_ws (gram_tc_gather_bytes).
 size_t gram_tc_gather_bytes(uint32_t k, uint64_t wpm);
 cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t wpm,

@@ -586,6 +586,99 @@ cudaError_t launch_overlap(const OverlapArgs &a_in, cudaStream_t s) {
   return launch_overlap_t<false, 12>(tm, a, sbins, ntg, s);
 }
 
+// ---------------------------------------------------------------------------
+// Multi-panel fused recompute, second half: counts = sum of the panels' uint16 partial
+// counts; composite from the SMEM grey table; histogram run-length into SMEM bins.
+// 24 B/px of traffic (4 panels) instead of the N/8 B/px re-read of the packed masks.
+// ---------------------------------------------------------------------------
+constexpr int kCombThreads = 256;
+__global__ void __launch_bounds__(kCombThreads)
+    k_combine_partials(const uint16_t *__restrict__ part, uint32_t npanels, uint64_t pitch,
+                       const OverlapArgs a, uint32_t sbins) {
+  extern __shared__ uint32_t csm[];
+  uint32_t *hist = csm;            // sbins (0 -> global atomics)
+  uint32_t *lut = csm + sbins;     // sbins RGBA words
+  for (uint32_t i = threadIdx.x; i < sbins; i += blockDim.x) {
+    hist[i] = 0;
+    lut[i] = (a.rgba != nullptr && i < a.nbins) ? rgba_word(i, a.n_inputs, a.lut) : 0u;
+  }
+  __syncthreads();
+  const uint64_t ngroups = (a.pixels + 7) / 8;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < ngroups; g += stride) {
+    const uint64_t p0 = g * 8;
+    uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t q = 0; q < npanels; ++q) {
+      const uint4 v = ptx::ld_nc_v4(part + q * pitch + p0);  // pitch is a multiple of 1024
+      c[0] += v.x & 0xFFFFu; c[1] += v.x >> 16;
+      c[2] += v.y & 0xFFFFu; c[3] += v.y >> 16;
+      c[4] += v.z & 0xFFFFu; c[5] += v.z >> 16;
+      c[6] += v.w & 0xFFFFu; c[7] += v.w >> 16;
+    }
+    const int nv = a.pixels - p0 >= 8 ? 8 : (int)(a.pixels - p0);
+    if (a.bins != nullptr) {
+      uint32_t cur = c[0], run = 1;
+      for (int j = 1; j < nv; ++j) {
+        if (c[j] != cur) {
+          if (sbins) atomicAdd(hist + cur, run);
+          else atomicAdd(a.bins + cur, (unsigned long long)run);
+          cur = c[j];
+          run = 0;
+        }
+        ++run;
+      }
+      if (sbins) atomicAdd(hist + cur, run);
+      else atomicAdd(a.bins + cur, (unsigned long long)run);
+    }
+    uint32_t r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      r[j] = a.rgba == nullptr ? 0u : (sbins ? lut[c[j]] : rgba_word(c[j], a.n_inputs, a.lut));
+    if (nv == 8 && a.vec) {
+      if (a.counts) {
+        st_cs_v4(a.counts + p0, make_uint4(c[0], c[1], c[2], c[3]));
+        st_cs_v4(a.counts + p0 + 4, make_uint4(c[4], c[5], c[6], c[7]));
+      }
+      if (a.rgba) {
+        st_cs_v4(a.rgba + p0, make_uint4(r[0], r[1], r[2], r[3]));
+        st_cs_v4(a.rgba + p0 + 4, make_uint4(r[4], r[5], r[6], r[7]));
+      }
+    } else {
+      for (int j = 0; j < nv; ++j) {
+        if (a.counts) a.counts[p0 + j] = c[j];
+        if (a.rgba) a.rgba[p0 + j] = r[j];
+      }
+    }
+  }
+  if (sbins && a.bins != nullptr) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < sbins && i < a.nbins; i += blockDim.x)
+      if (hist[i]) atomicAdd(a.bins + i, (unsigned long long)hist[i]);
+  }
+}
+
+cudaError_t launch_combine_partials(const uint16_t *partial16, uint32_t npanels, uint64_t pitch,
+                                    const OverlapArgs &a_in, cudaStream_t s) {
+  if (a_in.pixels == 0) return cudaSuccess;
+  OverlapArgs a = a_in;
+  a.vec = ((reinterpret_cast<uintptr_t>(a.counts) | reinterpret_cast<uintptr_t>(a.rgba)) & 15) == 0;
+  const uint32_t sbins = a.nbins <= 8192 ? (uint32_t)((a.nbins + 31) / 32 * 32) : 0u;
+  const size_t smem = (size_t)sbins * 8;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && attr < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_combine_partials,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  const uint64_t ngroups = (a.pixels + 7) / 8;
+  uint64_t grid = (ngroups + kCombThreads - 1) / kCombThreads;
+  const uint64_t gcap = (uint64_t)num_sms() * 8;
+  if (grid > gcap) grid = gcap;
+  k_combine_partials<<<(unsigned)grid, kCombThreads, smem, s>>>(partial16, npanels, pitch, a, sbins);
+  return cudaGetLastError();
+}
+
 // Per-item streaming accumulate (run_stream's kernel[i]): counts += bits of one
 // mask.  A warp takes one tile: one coalesced 128-B load, then word i is broadcast
 // and lane l adds bit l, so the counts stores are lane-contiguous.
@@ -821,9 +914,17 @@ __global__ void k_similarity(const long long *__restrict__ gram, uint32_t n, dou
 __global__ void k_outliers(const double *__restrict__ sim, uint32_t n, double *__restrict__ scores) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  // loads are batched 16 ahead of the (strictly sequential) additions
   double acc = 0.0;
-  for (uint32_t j = 0; j < n; ++j)
-    if (j != i) acc = __dadd_rn(acc, sim[(uint64_t)j * n + i]);
+  for (uint32_t j0 = 0; j0 < n; j0 += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      v[u] = j0 + u < n ? sim[(uint64_t)(j0 + u) * n + i] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (j0 + u < n && j0 + u != i) acc = __dadd_rn(acc, v[u]);
+  }
   scores[i] = __dsub_rn(1.0, __ddiv_rn(acc, (double)(n - 1)));
 }
 
