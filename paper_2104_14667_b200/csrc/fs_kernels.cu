@@ -909,23 +909,31 @@ __global__ void k_similarity(const long long *__restrict__ gram, uint32_t n, dou
 }
 
 // Row i's sum walks column i instead (sim is exactly symmetric: the Gram is mirrored
-// and inter / (g_ii + g_jj - inter) is the same double either way), so at step j the
-// threads of a warp read consecutive addresses.
-__global__ void k_outliers(const double *__restrict__ sim, uint32_t n, double *__restrict__ scores) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  // loads are batched 16 ahead of the (strictly sequential) additions
+// and inter / (g_ii + g_jj - inter) is the same double either way).  A warp owns 32
+// consecutive rows: it stages 128 x 32 blocks of the matrix in SMEM with independent,
+// coalesced loads (lane l reads column i0 + l of each row j), then every lane adds its
+// column in ascending j — the reference's order, so the sums are bit-identical.
+constexpr int kOutJ = 128;
+__global__ void __launch_bounds__(32)
+    k_outliers(const double *__restrict__ sim, uint32_t n, double *__restrict__ scores) {
+  __shared__ double tile[kOutJ][33];
+  const uint32_t lane = threadIdx.x;
+  const uint32_t i = blockIdx.x * 32 + lane;
   double acc = 0.0;
-  for (uint32_t j0 = 0; j0 < n; j0 += 16) {
-    double v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u)
-      v[u] = j0 + u < n ? sim[(uint64_t)(j0 + u) * n + i] : 0.0;
-#pragma unroll
-    for (int u = 0; u < 16; ++u)
-      if (j0 + u < n && j0 + u != i) acc = __dadd_rn(acc, v[u]);
+  for (uint32_t j0 = 0; j0 < n; j0 += kOutJ) {
+#pragma unroll 8
+    for (int r = 0; r < kOutJ; ++r) {
+      const uint32_t j = j0 + r;
+      tile[r][lane] = (j < n && i < n) ? sim[(uint64_t)j * n + i] : 0.0;
+    }
+    __syncwarp();
+    for (int r = 0; r < kOutJ; ++r) {
+      const uint32_t j = j0 + r;
+      if (j < n && j != i) acc = __dadd_rn(acc, tile[r][lane]);
+    }
+    __syncwarp();
   }
-  scores[i] = __dsub_rn(1.0, __ddiv_rn(acc, (double)(n - 1)));
+  if (i < n) scores[i] = __dsub_rn(1.0, __ddiv_rn(acc, (double)(n - 1)));
 }
 
 cudaError_t launch_similarity_outliers(const long long *gram, uint32_t n, double *sim,
