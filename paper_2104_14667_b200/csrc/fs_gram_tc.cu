@@ -811,18 +811,38 @@ struct Plan {
   uint64_t upc_diag, upc_off;
 };
 
-static void chunking(uint64_t total_units, uint32_t ntiles, int num_sms, uint32_t &kc,
+// K chunks per tile: the grid is ntiles * kc CTAs (or CTA pairs) over `slots` resident
+// positions.  Pick the kc that keeps the machine busiest over whole waves,
+// ntiles*kc / (waves * slots), preferring fewer chunks on ties (less prologue and
+// partial-reduce work); a chunk keeps >= 32 units (32 K px) and respects max_upc
+// (the FP4 exactness cap).
+static void chunking(uint64_t total_units, uint32_t ntiles, int slots, uint32_t &kc,
                      uint64_t &upc, uint64_t max_upc = UINT64_MAX) {
   if (ntiles == 0 || total_units == 0) {
     kc = 0;
     upc = 0;
     return;
   }
-  // chunks per tile: as many as keep ntiles * chunks within one wave of num_sms CTAs
-  uint64_t want = (uint64_t)num_sms / ntiles;
-  if (want < 1) want = 1;
-  if (want > total_units) want = total_units;
-  upc = (total_units + want - 1) / want;
+  const uint64_t S = (uint64_t)(slots > 0 ? slots : 1);
+  const uint64_t kc_min = (total_units + max_upc - 1) / max_upc;  // exactness cap
+  uint64_t kc_max = std::max<uint64_t>(kc_min, std::min<uint64_t>(total_units / 32, 8 * S));
+  if (kc_max < 1) kc_max = 1;
+  double best_eff = -1.0;
+  uint64_t best = kc_min > 0 ? kc_min : 1;
+  for (uint64_t c = (kc_min > 0 ? kc_min : 1); c <= kc_max; ++c) {
+    const uint64_t u = (total_units + c - 1) / c;  // units per chunk
+    const uint64_t real = (total_units + u - 1) / u;  // chunks actually used
+    if (real != c) continue;
+    const uint64_t ctas = (uint64_t)ntiles * c;
+    const uint64_t waves = (ctas + S - 1) / S;
+    const double eff = (double)ctas / (double)(waves * S);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best = c;
+    }
+    if (waves > 4) break;  // deeper than a few waves buys nothing
+  }
+  upc = (total_units + best - 1) / best;
   if (upc > max_upc) upc = max_upc;
   kc = (uint32_t)((total_units + upc - 1) / upc);
 }
