@@ -814,7 +814,7 @@ struct Plan {
 // K chunks per tile: the grid is ntiles * kc CTAs (or CTA pairs) over `slots` resident
 // positions.  Pick the kc that keeps the machine busiest over whole waves,
 // ntiles*kc / (waves * slots), preferring fewer chunks on ties (less prologue and
-// partial-reduce work); a chunk keeps >= 32 units (32 K px) and respects max_upc
+// partial-reduce work); a chunk keeps >= 4 units (4 K px) and respects max_upc
 // (the FP4 exactness cap).
 static void chunking(uint64_t total_units, uint32_t ntiles, int slots, uint32_t &kc,
                      uint64_t &upc, uint64_t max_upc = UINT64_MAX) {
@@ -825,7 +825,7 @@ static void chunking(uint64_t total_units, uint32_t ntiles, int slots, uint32_t 
   }
   const uint64_t S = (uint64_t)(slots > 0 ? slots : 1);
   const uint64_t kc_min = (total_units + max_upc - 1) / max_upc;  // exactness cap
-  uint64_t kc_max = std::max<uint64_t>(kc_min, std::min<uint64_t>(total_units / 32, 8 * S));
+  uint64_t kc_max = std::max<uint64_t>(kc_min, std::min<uint64_t>(total_units / 4, 8 * S));
   if (kc_max < 1) kc_max = 1;
   double best_eff = -1.0;
   uint64_t best = kc_min > 0 ? kc_min : 1;
