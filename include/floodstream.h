@@ -161,7 +161,7 @@ int fs_ensemble_stream_handle(fs_ensemble *ens, void **stream);
 int fs_ensemble_set_stream(fs_ensemble *ens, void *stream);
 /* Blocks until all work queued on the ensemble's streams has finished. */
 int fs_ensemble_sync(fs_ensemble *ens);
-/* Choose the Gram engine used by FS_GRAM_AUTO (process-wide). */
+/* Choose the Gram engine used by FS_GRAM_AUTO (process-wide; default FS_GRAM_TC_F4). */
 int fs_set_gram_engine(int engine);
 /* Choose the transform kernel: 0 = TMA bulk-staged, 1 = direct vector loads,
  * 2 = 8 coalesced 16-B loads in flight per thread (4 KB per warp). */

@@ -212,7 +212,9 @@ static int get_ctx(ThreadCtx **out) {
   return FS_OK;
 }
 
-static std::atomic<int> g_gram_engine{FS_GRAM_TC_I8};
+// default for FS_GRAM_AUTO: the fastest measured engine (kind::mxf4 diagonal tiles,
+// CTA-pair mxf4 off-diagonal tiles, fused overlap pass)
+static std::atomic<int> g_gram_engine{FS_GRAM_TC_F4};
 
 static int num_sms_cached() {
   int dev = 0, n = 0;
