@@ -491,3 +491,21 @@ def test_device_similarity_and_outliers_bitwise(k):
         want = O.outlier_scores(sim, ids)
         got = d_o.cpu().numpy()
         assert [float(x).hex() for x in got] == [float(want[i]).hex() for i in ids]
+
+
+def test_error_mapping_on_device():
+    """C-ABI status codes surface as the reference's error kinds: bad arguments ->
+    ValueError, device allocation failure -> MemoryError; the handle stays usable."""
+    cells = [synth_cells(64, 32, i, members=2) for i in range(3)]
+    with DeviceEnsemble(64, 32, 3) as ens:
+        ens.upload(cells)
+        with pytest.raises(ValueError, match="slot"):
+            ens.overlap([0, 3])
+        with pytest.raises(ValueError):
+            ens.stream(cells + cells, first=1)
+        with pytest.raises(ValueError):
+            ens.products([])
+        c, _, _ = ens.overlap()
+        assert np.array_equal(c, O.accumulate(cells, 64, 32))
+    with pytest.raises(MemoryError):
+        DeviceEnsemble(1 << 20, 1 << 16, 4096)  # 2^36 px x 4096 masks: far beyond 180 GB
