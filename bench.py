@@ -228,7 +228,9 @@ def reference_arm(args, width, height, k, members, eps, rank, world):
     kind = "reference" if getattr(mod, "NAME", "") == "cython" else "port"
     cores = os.cpu_count() or 1
     P = width * height
-    rows_per_worker = 8
+    # bounded sample per step, sized so the whole --steps K --warmup W run stays within a
+    # few minutes: 8 rows of every mask per worker at K + W <= 20, down to 1 row
+    rows_per_worker = max(1, min(8, round(160 / max(1, args.steps + args.warmup))))
     window_rows = rows_per_worker * cores
     rng = np.random.default_rng(0)
     npairs_total = k * (k - 1) // 2

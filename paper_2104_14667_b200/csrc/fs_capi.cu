@@ -41,6 +41,10 @@ static int set_err(int code, const std::string &msg) {
   return code;
 }
 static int cuda_err(cudaError_t e, const char *what) {
+  // consume the runtime's per-thread "last error" too: a non-sticky failure (e.g. an
+  // allocation that did not fit) must not resurface from the next launch's
+  // cudaGetLastError() check
+  cudaGetLastError();
   if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
     return set_err(FS_ENODEV, std::string(what) + ": " + cudaGetErrorString(e));
   if (e == cudaErrorMemoryAllocation)

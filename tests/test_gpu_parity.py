@@ -509,3 +509,31 @@ def test_error_mapping_on_device():
         assert np.array_equal(c, O.accumulate(cells, 64, 32))
     with pytest.raises(MemoryError):
         DeviceEnsemble(1 << 20, 1 << 16, 4096)  # 2^36 px x 4096 masks: far beyond 180 GB
+
+
+def test_concurrent_callers():
+    """The reference calls the primitives from its recompute worker, the request
+    threadpool and job threads at once (service.py:92-95,198,289-324): protocol calls
+    from 6 threads plus shared-ensemble recomputes stay exact."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    w, h, k = 300, 97, 12
+    cells = [synth_cells(w, h, i, members=3, eps=0.05) for i in range(k)]
+    want_counts = O.accumulate(cells, w, h)
+    want_gram = O.gram(cells)
+    surfaces = surfaces_of(cells)
+    with DeviceEnsemble(w, h, k) as ens:
+        ens.upload(cells)
+
+        def job(t):
+            if t % 3 == 0:
+                g = fs.accumulate(surfaces)
+                return np.array_equal(g.counts, want_counts)
+            if t % 3 == 1:
+                c, b, r, g, _ = ens.products(engine="tc-f4")
+                return np.array_equal(c, want_counts) and np.array_equal(g, want_gram)
+            a, b = cells[t % k].reshape(-1), cells[(t + 1) % k].reshape(-1)
+            return K.pair_counts(a, b) == O.pair_counts(a, b)
+
+        with ThreadPoolExecutor(max_workers=6) as pool:
+            assert all(pool.map(job, range(36)))
