@@ -448,7 +448,8 @@ def test_c3_scale_gram_and_clusters():
         O.cluster(sim[np.ix_(sub, sub)], [ids[i] for i in sub], 0.8)
 
 
-@pytest.mark.parametrize("k,h,w", [(520, 30, 70), (300, 1100, 1536)])
+@pytest.mark.parametrize("k,h,w", [(520, 30, 70), (300, 1100, 1536), (1100, 9, 100),
+                                   (4096, 4, 64)])
 def test_gram_pair_kernel_multi_panel(k, h, w):
     """k > 256: off-diagonal 256 x 256 tiles run on CTA pairs (cta_group::2, mxf4);
     several panels and many K chunks against the CUDA-core engine and the oracle."""
@@ -461,8 +462,14 @@ def test_gram_pair_kernel_multi_panel(k, h, w):
         ens.upload(cells)
         got = ens.gram(engine="tc-f4")
         ref = ens.gram(engine="popc")
-    assert np.array_equal(got, ref)
-    if h * w <= 100_000:
+        c, b, r, g2, fused = ens.products(engine="tc-f4")  # multi-panel fused recompute
+    assert fused
+    assert np.array_equal(got, ref) and np.array_equal(g2, ref)
+    counts = O.accumulate(cells, w, h)
+    assert np.array_equal(c, counts)
+    assert b.tolist() == O.overlap_counts(counts.reshape(-1), k).tolist()
+    assert np.array_equal(r, O.composite(counts, k))
+    if h * w <= 100_000 and k <= 1100:
         assert np.array_equal(got, O.gram(cells))
 
 

@@ -29,7 +29,8 @@ def main():
         peaks = json.loads(p.read_text())
     hbm = float(peaks.get("hbm_gbs", 6550.0))
     cases = [(16, 1024, 1024), (64, 4096, 4096), (128, 8192, 8192), (256, 8192, 8192),
-             (384, 8192, 5461), (512, 8192, 4096), (1024, 4096, 4096), (2048, 4096, 2048)]
+             (384, 8192, 5461), (512, 8192, 4096), (1024, 4096, 4096), (2048, 4096, 2048),
+             (4096, 4096, 1024)]
     for k, w, h in cases:
         P = w * h
         with DeviceEnsemble(w, h, k) as ens:
