@@ -702,7 +702,8 @@ def main():
         t_min = h2d / (pcie * 1e9)
         e2e = {"value": round(k * P * args.e2e_steps / t_e2e / 1e9, 4), "unit": UNIT,
                "h2d_bytes_per_step": int(k * P),
-               "d2h_bytes_per_step": int(8 * P + world * 8 * ((k + 1) + k * k)),
+               # counts + RGBA of every band, and per rank [bins | Gram] + Jaccard + scores
+               "d2h_bytes_per_step": int(8 * P + world * 8 * ((k + 1) + 2 * k * k + k)),
                "ms_per_step": round(t_e2e / args.e2e_steps * 1e3, 3),
                "fps": round(args.e2e_steps / t_e2e, 4), "steps": args.e2e_steps,
                "roofline": {"bound": "pcie_h2d", "achieved": round(h2d / (t_e2e / args.e2e_steps) / 1e9, 2),
