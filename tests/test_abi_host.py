@@ -240,3 +240,19 @@ def test_clustering_components_with_cross_block_ties(seed):
     ids = [f"s{v % (k - 1 if seed % 2 else k):03d}" for v in rng.permutation(k)]
     for tau in (0.8, 0.85, 0.9, 1.0):
         assert cluster_from_similarity(sim, ids, tau) == O.cluster(sim, ids, tau)
+
+
+def test_bench_cli_fails_cleanly_without_gpu():
+    """python -m paper_2104_14667_b200 bench <suite> (the reference's `bench` suites,
+    fs/cli.py:72-150): exit code 2 and a message when no device is visible."""
+    import subprocess
+    import sys
+
+    from paper_2104_14667_b200 import _native as N
+
+    if N.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    r = subprocess.run([sys.executable, "-m", "paper_2104_14667_b200", "bench", "backends",
+                        "--pixels", "4096", "--surfaces", "2", "--repeats", "1"],
+                       capture_output=True, text=True, cwd=REPO, timeout=120)
+    assert r.returncode == 2 and r.stderr.startswith("error:")

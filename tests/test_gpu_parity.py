@@ -544,3 +544,25 @@ def test_concurrent_callers():
 
         with ThreadPoolExecutor(max_workers=6) as pool:
             assert all(pool.map(job, range(36)))
+
+
+def test_bench_cli_suites(tmp_path):
+    """The measured `bench` suites through the module CLI (fs/cli.py:72-150 shape)."""
+    import json as _json
+    import subprocess
+    import sys
+
+    for argv, out in ([["backends", "--pixels", "65536", "--surfaces", "3", "--repeats", "1"],
+                       "b.json"],
+                      [["dual", "--dims", "96x64", "--n", "3", "--repeats", "1"], "d.csv"],
+                      [["transfer", "--min-bytes", "65536", "--max-bytes", "131072",
+                        "--step-bytes", "65536", "--repeats", "1"], "t.json"],
+                      [["sweep", "--start", "64", "--step", "500", "--stop", "1100", "--reps",
+                        "1"], "s.json"]):
+        p = tmp_path / out
+        r = subprocess.run([sys.executable, "-m", "paper_2104_14667_b200", "bench", *argv,
+                            "--out", str(p)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert p.exists() and p.stat().st_size > 0
+        if out.endswith(".json"):
+            _json.loads(p.read_text())
