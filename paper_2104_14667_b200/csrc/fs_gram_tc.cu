@@ -743,231 +743,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Diagonal 256-mask panels, FP4, operands loaded straight from global memory.
-//
-// The TMA-staged kernel above is bound by shared-memory bandwidth: per 256-px stage the
-// MMAs read 80 KB of operands, the expanders write 32 KB, and the raw tiles cost
-// another 8 KB (TMA write) + 8 KB (expander read) + 8 KB (counter read).  Here the raw
-// bits never touch SMEM: each expander thread keeps its own mask row's next stages in
-// registers (2 x 16-B ld.global.nc per stage, one 1024-px unit ahead), and the counter
-// warps read their 32 words per row with coalesced 128-B loads (L2 serves the second
-// touch).  SMEM traffic drops to 112 KB per stage (896 cycles vs 768 of MMA), and the
-// freed raw ring becomes 6-7 operand stages.  Everything else — MMA issue, TMEM layout,
-// epilogue, the fused overlap pass — is the kernel above.
-// ---------------------------------------------------------------------------
-constexpr int kLdgExpWarps = 8;
-constexpr int kLdgDepth = 4;  // stages of raw bits in flight per expander thread
-
-template <bool FUSE>
-struct LdgCfg {
-  static constexpr int kThreads = 32 * (1 + kLdgExpWarps + (FUSE ? 4 : 0));
-  static constexpr int kCnt0 = 1 + kLdgExpWarps;
-  static constexpr int kExtra = FUSE ? (4 * 32 * kTileTb * 4 + 2 * kFuseBins * 4) : 0;
-  static constexpr int kStageBytes = 256 * 128;
-  static constexpr int kStagesFit = (232448 - 1024 - 256 - kExtra) / kStageBytes;
-  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kExtra + 1024 + 256;
-};
-
-template <bool FUSE>
-__global__ void __launch_bounds__(LdgCfg<FUSE>::kThreads, 1)
-    k_gram_diag_ldg(const uint32_t *__restrict__ src, uint64_t cap, uint64_t rowbase,
-                    uint32_t krows, uint32_t kchunks, uint64_t units_per_chunk,
-                    uint64_t total_units, int32_t *__restrict__ partial, const OverlapArgs ov) {
-  using C = LdgCfg<FUSE>;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw_addr = ptx::smem_u32(smem_raw);
-  const uint32_t pad = (1024u - (raw_addr & 1023u)) & 1023u;
-  uint8_t *smem = smem_raw + pad;
-  const uint32_t op_base = raw_addr + pad;
-  uint8_t *extra = smem + C::kStages * C::kStageBytes;
-  uint32_t *cnt_tb = reinterpret_cast<uint32_t *>(extra);
-  uint32_t *sh_hist = cnt_tb + 4 * 32 * kTileTb;
-  uint32_t *sh_lut = sh_hist + kFuseBins;
-  uint64_t *full = reinterpret_cast<uint64_t *>(extra + C::kExtra);
-  uint64_t *empty = full + C::kStages;
-  uint64_t *tmem_full = empty + C::kStages;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const uint32_t I = blockIdx.x / kchunks;
-  const uint32_t kc = blockIdx.x % kchunks;
-  const uint64_t u0 = (uint64_t)kc * units_per_chunk;
-  const uint64_t u1 = min(u0 + units_per_chunk, total_units);
-  const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
-  const int nst = nunits * 4;
-
-  if (tid == 0) {
-    for (int q = 0; q < C::kStages; ++q) {
-      ptx::mbar_init(&full[q], kLdgExpWarps);
-      ptx::mbar_init(&empty[q], 1);
-    }
-    ptx::mbar_init(tmem_full, 1);
-    ptx::fence_mbar_init();
-  }
-  const bool lut_sh = FUSE && ov.rgba != nullptr;
-  if (FUSE && warp >= C::kCnt0) {
-    for (int i = tid - 32 * C::kCnt0; i < kFuseBins; i += 128) {
-      sh_hist[i] = 0;
-      sh_lut[i] = lut_sh && (uint32_t)i < ov.nbins ? rgba_word(i, ov.n_inputs, ov.lut) : 0u;
-    }
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     ptx::smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = *tmem_slot;
-  if (warp >= 1 && warp <= 4) {  // block scales = 1.0
-    const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
-    tmem_st16(tmem + lanes + kSfCol, kSfOnes);
-    tmem_st16(tmem + lanes + kSfCol + 16, kSfOnes);
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-
-  if (warp == 0) {
-    // ===== MMA issuer: rows 0-127 x N=256 and rows 128-255 x N=128 (3/4 of the square)
-    if (lane == 0 && nst > 0) {
-      constexpr uint32_t idA = idesc_mxf4(128, 256);
-      constexpr uint32_t idB = idesc_mxf4(128, 128);
-      const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 16;
-      for (int j = 0; j < nst; ++j) {
-        const int s = j % C::kStages;
-        ptx::mbar_wait(&full[s], (uint32_t)((j / C::kStages) & 1));
-        fence_after();
-        const uint32_t a_base = op_base + s * C::kStageBytes;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
-          mma_mxf4(tmem, sw128_desc(a_base + ks * 32), sw128_desc(a_base + ks * 32), idA, acc,
-                   sfa, sfb);
-          mma_mxf4(tmem + 256u, sw128_desc(a_base + 128 * 128 + ks * 32),
-                   sw128_desc(a_base + 128 * 128 + ks * 32), idB, acc, sfa, sfb);
-        }
-        mma_commit(&empty[s]);
-      }
-      mma_commit(tmem_full);
-    }
-    __syncwarp();
-  } else if (FUSE && warp >= C::kCnt0) {
-    // ===== counters: warp cw counts units cw, cw + 4, ... from global memory =====
-    const int cw = warp - C::kCnt0;
-    for (int u = cw; u < nunits; u += 4) {
-      const uint32_t *tile = src + ((u0 + (uint64_t)u) * cap + rowbase + (uint64_t)I * 256) * 32;
-      HSCounter<5> hc;
-      hc.reset();
-#pragma unroll 1
-      for (int g = 0; g < 256; g += 32) {
-        uint32_t d0[16], d1[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t r0 = (uint32_t)(g + j), r1 = (uint32_t)(g + 16 + j);
-          d0[j] = I * 256 + r0 < krows ? ptx::ld_nc_u32(tile + r0 * 32 + lane) : 0u;
-          d1[j] = I * 256 + r1 < krows ? ptx::ld_nc_u32(tile + r1 * 32 + lane) : 0u;
-        }
-        hc.add16(d0);
-        hc.add16(d1);
-      }
-      uint32_t cnt32[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) cnt32[j] = 0;
-      hc.extract(cnt32, 1u);
-      if (ov.partial16 != nullptr)
-        emit_partial16(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb,
-                       ov.partial16 + (uint64_t)I * ov.part_pitch);
-      else
-        emit_tile(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
-                  ov.bins != nullptr, sh_lut, lut_sh);
-    }
-  } else {
-    // ===== expanders: thread t owns mask row t of the panel =====
-    const uint32_t t = (uint32_t)(tid - 32);
-    const bool valid = I * 256 + t < krows;
-    const uint32_t *row = src + (rowbase + (uint64_t)I * 256 + t) * 32;
-    const uint64_t ustride = cap * 32;  // words between consecutive units of one row
-    uint4 buf[kLdgDepth][2];
-    auto fetch = [&](int j, uint4 (&v)[2]) {
-      if (valid && j < nst) {
-        const uint32_t *p = row + (u0 + (uint64_t)(j >> 2)) * ustride + (uint32_t)(j & 3) * 8;
-        v[0] = ptx::ld_nc_v4(p);
-        v[1] = ptx::ld_nc_v4(p + 4);
-      } else {
-        v[0] = v[1] = make_uint4(0, 0, 0, 0);
-      }
-    };
-#pragma unroll
-    for (int d = 0; d < kLdgDepth; ++d) fetch(d, buf[d]);
-    for (int jj = 0; jj < nst; jj += kLdgDepth) {
-#pragma unroll
-      for (int d = 0; d < kLdgDepth; ++d) {
-        const int j = jj + d;
-        if (j < nst) {
-          const int s = j % C::kStages;
-          if (j >= C::kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / C::kStages) - 1) & 1));
-          const uint32_t sbase = op_base + s * C::kStageBytes;
-          expand_row_f4(sbase, t, 0u, buf[d][0]);
-          expand_row_f4(sbase, t, 4u, buf[d][1]);
-          ptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&full[s]);
-          fetch(j + kLdgDepth, buf[d]);
-        }
-      }
-    }
-    // ===== epilogue (same tile layout as the TMA-staged kernel) =====
-    const uint32_t q = (uint32_t)(warp & 3);
-    const int cg = (warp - 1) / 4;
-    int32_t *out = partial + (uint64_t)blockIdx.x * 256 * 256;
-    if (nst > 0) {
-      ptx::mbar_wait(tmem_full, 0);
-      fence_after();
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint32_t orow = h * 128 + q * 32 + lane;
-      const int c_begin = h == 1 ? 128 : 0;
-      for (int c0 = c_begin + 32 * cg; c0 < 256; c0 += 64) {
-        uint32_t v[32];
-        const uint32_t col = h == 1 ? (256u + (uint32_t)(c0 - 128)) : (uint32_t)c0;
-        tmem_ld32(tmem + ((q * 32u) << 16) + col, v);
-        if (nst == 0) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = 0;
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = (uint32_t)__float2int_rn(__uint_as_float(v[e]));
-        }
-        int4 *dst = reinterpret_cast<int4 *>(out + (uint64_t)orow * 256 + c0);
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          dst[e] = make_int4((int)v[4 * e], (int)v[4 * e + 1], (int)v[4 * e + 2], (int)v[4 * e + 3]);
-      }
-    }
-    fence_before();
-  }
-  __syncthreads();
-  if (FUSE && warp >= C::kCnt0 && ov.bins != nullptr) {
-    for (uint32_t i = tid - 32 * C::kCnt0; i < ov.nbins; i += 128)
-      if (sh_hist[i]) atomicAdd(ov.bins + i, (unsigned long long)sh_hist[i]);
-    if (blockIdx.x == 0 && tid == 32 * C::kCnt0) {
-      const uint64_t padpx = total_units * 1024 - ov.pixels;
-      if (padpx) atomicAdd(ov.bins, (unsigned long long)(0ull - padpx));
-    }
-  }
-  if (warp == 0) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
 // Sum int32 partials over K chunks; scatter into the k x k Gram (both triangles).
 template <int PANEL>
 __global__ void k_gram_reduce(const int32_t *__restrict__ part_diag, uint32_t kc_diag,
@@ -1137,34 +912,6 @@ static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t 
 
 size_t gram_tc_gather_bytes(uint32_t k, uint64_t wpm) { return (size_t)k * wpm * 4; }
 
-// FS_DIAG_TMA=1 selects the TMA-staged diagonal kernel (A/B comparisons)
-static bool diag_tma() {
-  static const bool v = [] {
-    const char *e = std::getenv("FS_DIAG_TMA");
-    return e != nullptr && e[0] == '1';
-  }();
-  return v;
-}
-
-template <bool FUSE>
-static cudaError_t launch_diag_ldg(const uint32_t *src, uint64_t cap, uint64_t row0, uint32_t k,
-                                   const tc::Plan &p, int32_t *part, const OverlapArgs &ov,
-                                   cudaStream_t s) {
-  using C = tc::LdgCfg<FUSE>;
-  if (p.ndiag == 0 || p.kc_diag == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_gram_diag_ldg<FUSE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  tc::k_gram_diag_ldg<FUSE><<<p.ndiag * p.kc_diag, C::kThreads, C::kSmemBytes, s>>>(
-      src, cap, row0, k, p.kc_diag, p.upc_diag, p.units_diag, part, ov);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t wpm,
                            const uint32_t *slots, const uint32_t *host_slots, uint32_t k,
                            unsigned long long *gram, void *workspace, void *gather_ws,
@@ -1236,15 +983,7 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
     if (e != cudaSuccess) return e;
     if ((e = launch_one<128, false>(tm_off, p, part_off, none, s)) != cudaSuccess) return e;
   } else {
-    if (fp4 && !diag_tma()) {
-      // FP4 diagonal panels: raw bits straight from global memory (no SMEM staging)
-      if (fuse_now)
-        e = launch_diag_ldg<true>(src, src_cap, row0, k, p, part_diag, *fuse, s);
-      else if (fuse_multi)
-        e = launch_diag_ldg<true>(src, src_cap, row0, k, p, part_diag, ovp, s);
-      else
-        e = launch_diag_ldg<false>(src, src_cap, row0, k, p, part_diag, none, s);
-    } else if (fuse_now)
+    if (fuse_now)
       e = fp4 ? launch_one<256, true, true, true>(tm_diag, p, part_diag, *fuse, s)
               : launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s);
     else if (fuse_multi)
