@@ -483,13 +483,31 @@ int fs_ensemble_create(uint64_t pixels, uint32_t capacity, fs_ensemble **out) {
   e->wpm = words_for_pixels(pixels);
   e->capacity = capacity;
   e->num_sms = num_sms_cached();
-  CK(cudaMalloc(&e->packed, (size_t)capacity * e->wpm * 4));
-  CK(cudaMemset(e->packed, 0, (size_t)capacity * e->wpm * 4));
-  CK(cudaStreamCreateWithFlags(&e->sc, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&e->sk_own, cudaStreamNonBlocking));
+  // on any failure, release what was created so far (no leaked streams / memory)
+  auto fail = [&](cudaError_t err, const char *what) {
+    if (e->packed) cudaFree(e->packed);
+    if (e->sc) cudaStreamDestroy(e->sc);
+    if (e->sk_own) cudaStreamDestroy(e->sk_own);
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 2; ++j)
+        if (e->kev[i][j]) cudaEventDestroy(e->kev[i][j]);
+    return cuda_err(err, what);
+  };
+  cudaError_t err;
+  const size_t bytes = (size_t)capacity * e->wpm * 4;
+  if ((err = cudaMalloc(&e->packed, bytes)) != cudaSuccess) {
+    e->packed = nullptr;
+    return fail(err, "cudaMalloc(packed masks)");
+  }
+  if ((err = cudaMemset(e->packed, 0, bytes)) != cudaSuccess) return fail(err, "cudaMemset");
+  if ((err = cudaStreamCreateWithFlags(&e->sc, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(err, "cudaStreamCreate(copy)");
+  if ((err = cudaStreamCreateWithFlags(&e->sk_own, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(err, "cudaStreamCreate(compute)");
   e->sk = e->sk_own;
   for (int i = 0; i < 4; ++i)
-    for (int j = 0; j < 2; ++j) CK(cudaEventCreate(&e->kev[i][j]));
+    for (int j = 0; j < 2; ++j)
+      if ((err = cudaEventCreate(&e->kev[i][j])) != cudaSuccess) return fail(err, "cudaEventCreate");
   *out = e.release();
   return FS_OK;
 }
