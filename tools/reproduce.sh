@@ -1,0 +1,30 @@
+#!/usr/bin/env bash
+# Regenerate the measurements DESIGN.md quotes, on one B200 (run from the repo root,
+# e.g. through gpurun).  Outputs land in gpurun_out/reproduce/; copy what you want
+# judged into profiles/.
+set -euo pipefail
+O=gpurun_out/reproduce
+mkdir -p "$O"
+python -c "import __graft_entry__ as g; g.build()"
+python -c "import __graft_entry__ as g; g.smoke()"                          > "$O/smoke.log"
+python -m pytest tests -q -m gpu                                            > "$O/pytest_gpu.log"
+python bench.py                                                             > "$O/bench_c2.json"
+python bench.py --impl reference                                            > "$O/bench_c2_reference.json"
+python bench.py --config c1                                                 > "$O/bench_c1.json"
+python bench.py --config c3 --no-cpu                                        > "$O/bench_c3.json"
+python bench.py --config c4 --steps 3 --warmup 1                            > "$O/bench_c4.json"
+python tools/sweep_bench.py                                                 > "$O/sweep_c5.json"
+python tools/dual_bench.py                                                  > "$O/dual_buffer_suite.json"
+python tools/k_sweep.py                                                     > "$O/k_sweep.jsonl"
+python tools/service_bench.py                                               > "$O/service_c2.json"
+python tools/ingest_bench.py                                                > "$O/ingest.json"
+# kernel evidence: the launch list of the bench command and one full capture of the
+# dominant kernel (numbers printed under ncu are not bench values)
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$O/launches_c2.csv" \
+    python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu              > /dev/null
+ncu --set full --clock-control none --import-source on -k regex:k_gram_tc -s 2 -c 1 \
+    -o "$O/c2_recompute_fused" python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null
+for tool in memcheck racecheck synccheck; do
+  compute-sanitizer --tool "$tool" python tools/sanitize_cases.py           > "$O/$tool.log" 2>&1
+done
+echo "done: $O"
