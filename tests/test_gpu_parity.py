@@ -566,3 +566,35 @@ def test_bench_cli_suites(tmp_path):
         assert p.exists() and p.stat().st_size > 0
         if out.endswith(".json"):
             _json.loads(p.read_text())
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_randomized_overlap_and_products(seed):
+    """Randomised shapes against the oracle: k in 1..320, odd raster sizes, masks in
+    permuted / gathered slots of a larger ensemble, cycled inputs (weights w1 = c + 1
+    for the first `remainder` surfaces, c for the rest, streaming.py:417-425), and the
+    fused recompute on the same slots."""
+    rng = np.random.default_rng(900 + seed)
+    k = int(rng.integers(1, 321))
+    h, w = int(rng.integers(1, 40)), int(rng.integers(1, 300))
+    cap = k + int(rng.integers(0, 5))
+    cells = [(rng.random((h, w)) < rng.uniform(0.0, 1.0)).astype(np.uint8) *
+             rng.integers(1, 256, (h, w)).astype(np.uint8) for _ in range(k)]
+    slots = rng.permutation(cap)[:k].tolist()
+    cyc, rem = int(rng.integers(1, 4)), int(rng.integers(0, k + 1))
+    with DeviceEnsemble(w, h, cap) as ens:
+        for s, c in zip(slots, cells):
+            ens.upload([c], first=s)
+        c1, b1, r1 = ens.overlap(slots, cycles=cyc, remainder=rem)
+        c2, b2, r2, g2, _ = ens.products(slots, engine="tc-f4")
+    n = cyc * k + rem
+    seq = [cells[i % k] for i in range(n)]  # run_stream's cycling order
+    want = O.accumulate(seq, w, h)
+    assert np.array_equal(c1, want)
+    assert b1.tolist() == O.overlap_counts(want.reshape(-1), n).tolist()
+    assert np.array_equal(r1, O.composite(want, n))
+    once = O.accumulate(cells, w, h)
+    assert np.array_equal(c2, once)
+    assert b2.tolist() == O.overlap_counts(once.reshape(-1), k).tolist()
+    assert np.array_equal(r2, O.composite(once, k))
+    assert np.array_equal(g2, O.gram(cells))
