@@ -532,7 +532,7 @@ constexpr int kPairExpWarps = 8;   // thread t < 128 expands A-half row t, t >= 
 constexpr int kPairDepth = 2;      // raw units in flight per CTA
 constexpr int kPairRawUnit = 2 * 128 * 128;  // A half + B half, 1024 px (128 B) per row
 constexpr int kPairStageBytes = 2 * 128 * 128;  // A + B operand halves, 256 px per row
-constexpr int kPairStages = 4;
+constexpr int kPairStages = 5;
 constexpr int kPairSmemBytes = kPairDepth * kPairRawUnit + kPairStages * kPairStageBytes + 1024 + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
