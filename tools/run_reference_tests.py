@@ -18,7 +18,6 @@ from __future__ import annotations
 
 import json
 import sys
-import types
 from pathlib import Path
 
 REPO = Path(__file__).resolve().parent.parent
@@ -32,17 +31,18 @@ def bind_floodstream() -> None:
     import paper_2104_14667_b200.backends as backends
     import paper_2104_14667_b200.rasters as rasters
 
+    import importlib.util
+
     pkg_dir = REF / "floodstream"
-    pkg = types.ModuleType("floodstream")
-    pkg.__path__ = [str(pkg_dir)]
-    pkg.__file__ = str(pkg_dir / "__init__.py")
-    pkg.__package__ = "floodstream"
+    # a real package spec (importlib.resources reads the bundled profiles through it)
+    spec = importlib.util.spec_from_file_location(
+        "floodstream", pkg_dir / "__init__.py", submodule_search_locations=[str(pkg_dir)])
+    pkg = importlib.util.module_from_spec(spec)
     sys.modules["floodstream"] = pkg
     for name, mod in (("analytics", analytics), ("backends", backends), ("rasters", rasters)):
         sys.modules[f"floodstream.{name}"] = mod
         setattr(pkg, name, mod)
-    code = compile((pkg_dir / "__init__.py").read_text(), str(pkg_dir / "__init__.py"), "exec")
-    exec(code, pkg.__dict__)
+    spec.loader.exec_module(pkg)
 
 
 class Collector:
