@@ -1,0 +1,32 @@
+"""The reference's own test suite, unmodified, with this package bound in as
+floodstream.analytics / .backends / .rasters (tools/run_reference_tests.py).  Needs the
+git-ignored reference install in baseline/_ref (pip --no-deps, offline) — skipped when it
+is absent.  Every hot-path file must pass; the only tolerated failure is the one the
+reference itself has on Python 3.12 (test_analytics_match_brute_force: the test sums
+Python floats with 3.12's compensated sum(), outlier_scores sums np.float64 — SURVEY §8c)."""
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = Path(__file__).resolve().parent.parent
+KNOWN = {"test_acceptance.py::test_analytics_match_brute_force"}
+HOT = ("test_analytics.py", "test_properties.py", "test_streaming.py", "test_service.py",
+       "test_rasters.py")
+
+
+def test_reference_suite_unmodified():
+    if not (REPO / "baseline" / "_ref" / "ref_tests").exists():
+        pytest.skip("reference install (baseline/_ref) not present")
+    r = subprocess.run([sys.executable, str(REPO / "tools" / "run_reference_tests.py")],
+                       capture_output=True, text=True, timeout=1200, cwd=REPO)
+    summary = json.loads(r.stdout.strip().splitlines()[-1])
+    assert set(summary["failed"]) <= KNOWN, summary["failed"]
+    for f in HOT:
+        assert summary["files"][f]["failed"] == 0 and summary["files"][f]["passed"] > 0, f
+    assert summary["passed"] >= 229
