@@ -12,7 +12,7 @@ B200 kernels; everything off the path (cost model, simulator, calibration, stats
 stays the reference's own code.  Prints one JSON summary line (per-file outcomes and the
 failing test ids) after pytest's own report.
 
-Usage: python tools/run_reference_tests.py [pytest args ...]
+Usage: python tools/run_reference_tests.py [--boundary-only] [pytest args ...]
 """
 from __future__ import annotations
 
@@ -24,12 +24,18 @@ REPO = Path(__file__).resolve().parent.parent
 REF = REPO / "baseline" / "_ref"
 
 
-def bind_floodstream() -> None:
-    """Make ``import floodstream`` = the reference package with our hot-path modules."""
+def bind_floodstream(boundary_only: bool = False) -> dict:
+    """Make ``import floodstream`` = the reference package with our hot-path modules.
+    ``boundary_only``: bind just the backend registry (fs/backends.py:21-47), so the
+    reference's OWN analytics.py drives our C-ABI protocol module primitive by primitive
+    (INTEGRATION.md §B)."""
     sys.path.insert(0, str(REPO))
     import paper_2104_14667_b200.analytics as analytics
     import paper_2104_14667_b200.backends as backends
     import paper_2104_14667_b200.rasters as rasters
+
+    bound = {"backends": backends} if boundary_only else {
+        "analytics": analytics, "backends": backends, "rasters": rasters}
 
     import importlib.util
 
@@ -39,10 +45,11 @@ def bind_floodstream() -> None:
         "floodstream", pkg_dir / "__init__.py", submodule_search_locations=[str(pkg_dir)])
     pkg = importlib.util.module_from_spec(spec)
     sys.modules["floodstream"] = pkg
-    for name, mod in (("analytics", analytics), ("backends", backends), ("rasters", rasters)):
+    for name, mod in bound.items():
         sys.modules[f"floodstream.{name}"] = mod
         setattr(pkg, name, mod)
     spec.loader.exec_module(pkg)
+    return {f"floodstream.{n}": m.__name__ for n, m in bound.items()}
 
 
 class Collector:
@@ -64,19 +71,20 @@ def main(argv: list[str]) -> int:
     if not (REF / "floodstream").exists() or not (REF / "ref_tests").exists():
         print(json.dumps({"unavailable": "baseline/_ref (reference install + ref_tests) missing"}))
         return 0
-    bind_floodstream()
+    boundary_only = "--boundary-only" in argv
+    argv = [a for a in argv if a != "--boundary-only"]
+    binding = bind_floodstream(boundary_only)
     import floodstream
 
-    assert floodstream.analytics.__name__ == "paper_2104_14667_b200.analytics"
+    assert floodstream.backends.__name__ == "paper_2104_14667_b200.backends"
+    assert floodstream.analytics.kernels.NAME == "cuda"
     import pytest
 
     col = Collector()
     args = [str(REF / "ref_tests"), "-q", "-p", "no:cacheprovider", "--rootdir",
             str(REF / "ref_tests")] + argv
     rc = pytest.main(args, plugins=[col])
-    print(json.dumps({"binding": {"floodstream.analytics": "paper_2104_14667_b200.analytics",
-                                  "floodstream.backends": "paper_2104_14667_b200.backends",
-                                  "floodstream.rasters": "paper_2104_14667_b200.rasters"},
+    print(json.dumps({"binding": binding,
                       "files": col.outcomes,
                       "passed": sum(d.get("passed", 0) for d in col.outcomes.values()),
                       "failed": col.failed}))
