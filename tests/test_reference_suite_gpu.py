@@ -20,10 +20,13 @@ HOT = ("test_analytics.py", "test_properties.py", "test_streaming.py", "test_ser
        "test_rasters.py")
 
 
-def test_reference_suite_unmodified():
+@pytest.mark.parametrize("mode", [[], ["--boundary-only"]])
+def test_reference_suite_unmodified(mode):
+    """mode []: our analytics/backends/rasters bound in; --boundary-only: only the
+    backend registry, so the reference's own analytics.py drives our protocol module."""
     if not (REPO / "baseline" / "_ref" / "ref_tests").exists():
         pytest.skip("reference install (baseline/_ref) not present")
-    r = subprocess.run([sys.executable, str(REPO / "tools" / "run_reference_tests.py")],
+    r = subprocess.run([sys.executable, str(REPO / "tools" / "run_reference_tests.py"), *mode],
                        capture_output=True, text=True, timeout=1200, cwd=REPO)
     summary = json.loads(r.stdout.strip().splitlines()[-1])
     assert set(summary["failed"]) <= KNOWN, summary["failed"]
