@@ -26,7 +26,10 @@ from .analytics import (
     similarity_matrix,
 )
 from .backends import available_backends, select_backend
+from .banded import BandedStream
+from .engine import AnalyticsEngine, EngineSnapshot, ResidentEngine, SlotMap
 from .ensemble import DeviceEnsemble, Snapshot, StreamStats
+from .ingest import stream_files
 from .rasters import RasterError, RasterSurface, load_surface
 from .schedule import Channel, OpKind, OpNode, ScheduleError, ScheduleGraph
 from .streaming import (
@@ -47,10 +50,13 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AccumulationGrid",
+    "AnalyticsEngine",
     "AnalyticsError",
+    "BandedStream",
     "Channel",
     "CompositeImage",
     "DeviceEnsemble",
+    "EngineSnapshot",
     "KERNEL_VARIANTS",
     "OpKind",
     "OpNode",
@@ -58,8 +64,10 @@ __all__ = [
     "PipelineRunReport",
     "RasterError",
     "RasterSurface",
+    "ResidentEngine",
     "ScheduleError",
     "ScheduleGraph",
+    "SlotMap",
     "Snapshot",
     "StreamError",
     "StreamJob",
@@ -85,4 +93,5 @@ __all__ = [
     "select_backend",
     "similarity_from_gram",
     "similarity_matrix",
+    "stream_files",
 ]
