@@ -96,11 +96,9 @@ constexpr int kTileTb = 36;  // transpose row stride (words): 16-B aligned, conf
 // bins (or global bins); padding pixels past a.pixels are counted in bin 0 and must be
 // removed once by the caller.  Counts / RGBA: transposed through `tb` and written with
 // 16-B streaming stores.
-// sh_lut: RGBA words (uint32_t) or grey levels (uint8_t, the word is built on the fly).
-template <typename LutT>
 __device__ __forceinline__ void emit_tile(const uint32_t (&cnt32)[32], uint64_t tile, int lane,
                                           uint32_t *tb, const OverlapArgs &a, uint32_t *sh_hist,
-                                          bool hist_sh, const LutT *sh_lut, bool lut_sh) {
+                                          bool hist_sh, const uint32_t *sh_lut, bool lut_sh) {
   if (a.bins != nullptr) {
     uint32_t cur = cnt32[0], run = 1;
 #pragma unroll
@@ -137,21 +135,10 @@ __device__ __forceinline__ void emit_tile(const uint32_t (&cnt32)[32], uint64_t 
     uint4 r = make_uint4(0, 0, 0, 0);
     if (a.rgba != nullptr) {
       if (lut_sh) {
-        if constexpr (sizeof(LutT) == 1) {
-          auto word = [&](uint32_t v) {
-            const uint32_t g = sh_lut[v];
-            return v == 0 ? 0u : (g | (g << 8) | 0xFFFF0000u);
-          };
-          r.x = word(c.x);
-          r.y = word(c.y);
-          r.z = word(c.z);
-          r.w = word(c.w);
-        } else {
-          r.x = sh_lut[c.x];
-          r.y = sh_lut[c.y];
-          r.z = sh_lut[c.z];
-          r.w = sh_lut[c.w];
-        }
+        r.x = sh_lut[c.x];
+        r.y = sh_lut[c.y];
+        r.z = sh_lut[c.z];
+        r.w = sh_lut[c.w];
       } else {
         r.x = rgba_word(c.x, a.n_inputs, a.lut);
         r.y = rgba_word(c.y, a.n_inputs, a.lut);

@@ -185,10 +185,7 @@ struct Cfg {
   // is counted by warp u % 4), so a counter warp only ever waits on its own slot, in
   // order, and can never run a full mbarrier phase ahead of it.
   static constexpr int kDepth = FUSE ? FD : kRawDepth;
-  // FUSE: SMEM histogram (uint32) + grey levels (uint8); the counter warps' transpose
-  // scratch lives in their own raw slot once the expanders are done with it, which
-  // leaves room for a third operand stage
-  static constexpr int kExtraBytes = FUSE ? (kFuseBins * 4 + kFuseBins) : 0;
+  static constexpr int kExtraBytes = FUSE ? (4 * 32 * kTileTb * 4 + 2 * kFuseBins * 4) : 0;
   static constexpr int kBudget = FUSE ? (232448 - 1024 - 256) : kSmemBudget;
   static constexpr int kRegions = DIAG ? 1 : 2;
   // 8 expander warps when there are >= 256 operand rows (latency hiding: each thread's
@@ -239,14 +236,14 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
   const uint32_t raw_base = smem_base;                                  // raw ring
   const uint32_t op_base = smem_base + kRawDepth * C::kRawUnitBytes;    // operand stages
   uint8_t *extra = smem + kRawDepth * C::kRawUnitBytes + C::kStages * C::kStageBytes;
-  uint32_t *sh_hist = reinterpret_cast<uint32_t *>(extra);     // FUSE: kFuseBins
-  uint8_t *sh_grey = extra + kFuseBins * 4;                      // FUSE: kFuseBins
-  uint64_t *full = reinterpret_cast<uint64_t *>(extra + ((C::kExtraBytes + 7) & ~7));
+  uint32_t *cnt_tb = reinterpret_cast<uint32_t *>(extra);        // FUSE: 4 x 32 x kTileTb
+  uint32_t *sh_hist = cnt_tb + 4 * 32 * kTileTb;                 // FUSE: kFuseBins
+  uint32_t *sh_lut = sh_hist + kFuseBins;                        // FUSE: kFuseBins
+  uint64_t *full = reinterpret_cast<uint64_t *>(extra + C::kExtraBytes);
   uint64_t *empty = full + C::kStages;
   uint64_t *raw_full = empty + C::kStages;
   uint64_t *raw_empty = raw_full + kRawDepth;
-  uint64_t *exp_done = raw_empty + kRawDepth;  // FUSE: expanders finished with the slot
-  uint64_t *tmem_full = exp_done + kRawDepth;
+  uint64_t *tmem_full = raw_empty + kRawDepth;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
   const int tid = threadIdx.x;
@@ -280,10 +277,7 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
     }
     for (int s = 0; s < kRawDepth; ++s) {
       ptx::mbar_init(&raw_full[s], 1);
-      // FUSE: the slot is released by its counter warp after the expanders are done
-      // (exp_done) and the counter used the slot as transpose scratch
-      ptx::mbar_init(&raw_empty[s], FUSE ? 32 : C::kExpThreads);
-      ptx::mbar_init(&exp_done[s], C::kExpThreads);
+      ptx::mbar_init(&raw_empty[s], FUSE ? C::kExpThreads + 32 : C::kExpThreads);
     }
     ptx::mbar_init(tmem_full, 1);
     ptx::fence_mbar_init();
@@ -292,8 +286,7 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
   if (FUSE && warp >= C::kCntWarp0) {
     for (int i = tid - 32 * C::kCntWarp0; i < kFuseBins; i += 128) {
       sh_hist[i] = 0;
-      sh_grey[i] = lut_sh && (uint32_t)i < ov.nbins ? (uint8_t)(rgba_word(i, ov.n_inputs, ov.lut) & 0xFFu)
-                                                     : (uint8_t)0;
+      sh_lut[i] = lut_sh && (uint32_t)i < ov.nbins ? rgba_word(i, ov.n_inputs, ov.lut) : 0u;
     }
   }
   if (warp == 0) {
@@ -403,22 +396,18 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
         }
         hc.add16(d);
       }
+      __syncwarp();
+      ptx::mbar_arrive(&raw_empty[ru]);
       uint32_t cnt32[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) cnt32[j] = 0;
       hc.extract(cnt32, 1u);
-      // the slot becomes this warp's transpose scratch once the expanders are done
-      ptx::mbar_wait(&exp_done[ru], (uint32_t)((u / kRawDepth) & 1));
-      uint32_t *tb = reinterpret_cast<uint32_t *>(smem + ru * C::kRawUnitBytes);
       if (ov.partial16 != nullptr)  // multi-panel: this panel's counts, summed later
-        emit_partial16(cnt32, u0 + (uint64_t)u, lane, tb, ov.partial16 + (uint64_t)I * ov.part_pitch);
+        emit_partial16(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb,
+                       ov.partial16 + (uint64_t)I * ov.part_pitch);
       else
-        emit_tile(cnt32, u0 + (uint64_t)u, lane, tb, ov, sh_hist, ov.bins != nullptr, sh_grey,
-                  lut_sh);
-      // the next TMA (async proxy) rewrites the scratch this warp wrote (generic proxy)
-      ptx::fence_proxy_async_smem();
-      __syncwarp();
-      ptx::mbar_arrive(&raw_empty[ru]);
+        emit_tile(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
+                  ov.bins != nullptr, sh_lut, lut_sh);
     }
   } else {
     // ===== expanders: raw bits (swizzled) -> 0/1 bytes in SW128 K-major operand =====
@@ -468,7 +457,7 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
       }
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&full[s]);
-      if (sub == C::kStagesPerUnit - 1) ptx::mbar_arrive(FUSE ? &exp_done[ru] : &raw_empty[ru]);
+      if (sub == C::kStagesPerUnit - 1) ptx::mbar_arrive(&raw_empty[ru]);
     }
     // ===== epilogue: TMEM -> registers -> int32 partial tile =====
     const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp
