@@ -120,3 +120,27 @@ def test_c4_full_size_banded_equals_resident():
     assert np.array_equal(r["bins"], bins_res)
     assert np.array_equal(r["gram"], gram_res)
     assert len(r["clusters"]) == k // members
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_banded_randomized(seed):
+    """Random geometry / band height / row block / k (incl. > 256) / source kind."""
+    rng = np.random.default_rng(4242 + seed)
+    k = int(rng.integers(1, 300))
+    w, h = int(rng.integers(1, 400)), int(rng.integers(1, 90))
+    row0 = int(rng.integers(0, h))
+    rows = int(rng.integers(1, h - row0 + 1))
+    band_rows = int(rng.integers(1, rows + 3))
+    cells = [(rng.random((h, w)) < rng.uniform(0, 1)).astype(np.uint8) *
+             rng.integers(1, 256, (h, w)).astype(np.uint8) for _ in range(k)]
+    with BandedStream(w, h, k, row0=row0, rows=rows, band_rows=band_rows) as bs:
+        if seed % 2:
+            r = bs.run(lambda i, r0, n: cells[i][row0 + r0:row0 + r0 + n], analytics=False)
+        else:
+            r = bs.run([c[row0:row0 + rows] for c in cells], analytics=False)
+    part = [c[row0:row0 + rows] for c in cells]
+    want = O.accumulate(part, w, rows)
+    assert np.array_equal(r["counts"], want)
+    assert np.array_equal(r["rgba"], O.composite(want, k))
+    assert r["bins"].tolist() == O.overlap_counts(want.reshape(-1), k).tolist()
+    assert np.array_equal(r["gram"], O.gram(part))

@@ -153,3 +153,22 @@ def test_resident_engine_beyond_one_panel():
         s2 = eng.compute(2, ws2, store.surface)
         assert s2.report["uploaded"] == 10
         _check(s2, store, ws2)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_resident_engine_random_working_sets(seed):
+    """A sequence of random working sets (growing, shrinking, reordered, evicting) on a
+    small-capacity engine: every snapshot equals the reference formulas."""
+    rng = np.random.default_rng(77 + seed)
+    store = FakeStore(64, 48, 40)
+    ids_all = sorted(store.cells)
+    with ResidentEngine(64, 48, 24) as eng:
+        for v in range(6):
+            n = int(rng.integers(1, 25))
+            ws = [ids_all[i] for i in rng.choice(40, n, replace=False)]
+            snap = eng.compute(v, ws, store.surface)
+            if n >= 2:
+                _check(snap, store, ws)
+            else:
+                assert snap.histogram == O.overlap_counts(
+                    O.accumulate([store.cells[ws[0]]], 64, 48).reshape(-1), 1).tolist()
