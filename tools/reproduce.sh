@@ -18,6 +18,8 @@ python tools/dual_bench.py                                                  > "$
 python tools/k_sweep.py                                                     > "$O/k_sweep.jsonl"
 python tools/service_bench.py                                               > "$O/service_c2.json"
 python tools/ingest_bench.py                                                > "$O/ingest.json"
+python tools/compare_with_reference.py                                      > "$O/compare_with_reference.json"
+python tools/run_reference_tests.py                                         > "$O/reference_suite.log" 2>&1
 # kernel evidence: the launch list of the bench command and one full capture of the
 # dominant kernel (numbers printed under ncu are not bench values)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$O/launches_c2.csv" \
