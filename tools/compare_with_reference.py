@@ -30,13 +30,14 @@ def main():
     if not (REF / "floodstream").exists():
         print(json.dumps({"unavailable": "baseline/_ref missing"}))
         return
-    os.environ["FLOODSTREAM_BACKEND"] = "numpy"
-    sys.path.insert(0, str(REF))
-    import floodstream as ref  # the reference package, unmodified
-
     sys.path.insert(0, str(REPO))
+    os.environ.pop("FLOODSTREAM_BACKEND", None)  # ours binds its "cuda" backend at import
     import paper_2104_14667_b200 as ours
     from paper_2104_14667_b200.synth import synth_cells
+
+    os.environ["FLOODSTREAM_BACKEND"] = "numpy"  # the reference binds numpy at import
+    sys.path.insert(0, str(REF))
+    import floodstream as ref  # the reference package, unmodified
 
     w, h, k = args.width, args.height, args.k
     cells = [synth_cells(w, h, i, members=args.members, eps=0.03) for i in range(k)]
