@@ -33,3 +33,16 @@ def test_reference_suite_unmodified(mode):
     for f in HOT:
         assert summary["files"][f]["failed"] == 0 and summary["files"][f]["passed"] > 0, f
     assert summary["passed"] >= 229
+
+
+def test_reference_implementation_outputs_identical():
+    """The reference implementation itself (baseline/_ref, NumPy backend) and the B200
+    path on one flood-like ensemble: digest, histogram, composite, similarity, outlier
+    float bits and cluster lists all identical (tools/compare_with_reference.py)."""
+    if not (REPO / "baseline" / "_ref" / "floodstream").exists():
+        pytest.skip("reference install (baseline/_ref) not present")
+    r = subprocess.run([sys.executable, str(REPO / "tools" / "compare_with_reference.py"),
+                        "--width", "640", "--height", "480", "--k", "40", "--members", "5"],
+                       capture_output=True, text=True, timeout=600, cwd=REPO)
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["all_identical"], out
