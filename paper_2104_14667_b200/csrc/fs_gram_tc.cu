@@ -225,7 +225,7 @@ template <int PANEL, bool DIAG, bool FP4, bool FUSE, int FD>
 __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal, 1)
     k_gram_tc(const __grid_constant__ CUtensorMap tm, uint32_t npanels, uint32_t kchunks,
               uint64_t units_per_chunk, uint64_t total_units, int32_t *__restrict__ partial,
-              const OverlapArgs ov, uint32_t krows) {
+              const OverlapArgs ov) {
   using C = Cfg<PANEL, DIAG, FP4, FUSE, FD>;
   constexpr int kRawDepth = C::kDepth;
   extern __shared__ uint8_t smem_raw[];
@@ -268,10 +268,6 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
   const uint64_t u1 = min(u0 + units_per_chunk, total_units);
   const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
   const int nst = nunits * C::kStagesPerUnit;
-  // a diagonal 256-panel holding <= 128 real masks (the tail panel of e.g. k = 384):
-  // only rows/cols 0..127 can be non-zero, so one M=128 x N=128 MMA per K step and no
-  // expansion of rows 128..255 (their Gram entries lie beyond k and are never read)
-  const bool half = DIAG && PANEL == 256 && krows - I * (uint32_t)PANEL <= 128u;
 
   if (tid == 0) {
     ptx::prefetch_tmap(&tm);
@@ -331,14 +327,6 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {  // 4 MMAs of 32 B of K per 128-B operand row
           const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
-          if (half) {
-            const uint64_t d = sw128_desc(a_base + ks * 32);
-            if (FP4)
-              mma_mxf4(tmem, d, d, idB, acc, sfa, sfb);
-            else
-              mma_i8(tmem, d, d, idB, acc);
-            continue;
-          }
 #pragma unroll
           for (int h = 0; h < C::kHalves; ++h) {
             const uint64_t adesc = sw128_desc(a_base + h * 128 * 128 + ks * 32);
@@ -458,7 +446,6 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
       for (int m = 0; m < C::kRowsPerThread; ++m) {
         const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
         const uint32_t r = idx / PANEL, rr = idx % PANEL;
-        if (half && rr >= 128u) continue;  // rows no MMA reads
         if (FP4) {
           // 32 raw bytes (256 px) -> the whole 128-B operand row
 #pragma unroll
@@ -817,7 +804,6 @@ __global__ void k_gather_slots(const uint32_t *__restrict__ packed, uint64_t cap
 
 struct Plan {
   int panel;
-  uint32_t k;  // masks (rows) in the Gram
   bool pair;  // off-diagonal tiles on CTA pairs (kind::mxf4, cta_group::2)
   uint32_t npanels, ndiag, noff;
   uint64_t units_diag, units_off;  // raw units along K for each tile kind
@@ -863,7 +849,6 @@ static void chunking(uint64_t total_units, uint32_t ntiles, int slots, uint32_t 
 
 static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms, bool fp4) {
   Plan p{};
-  p.k = k;
   p.panel = k <= 128 ? 128 : 256;
   p.npanels = (k + p.panel - 1) / p.panel;
   p.ndiag = p.npanels;
@@ -921,7 +906,7 @@ static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t 
   }
   tc::k_gram_tc<PANEL, DIAG, FP4, FUSE, FD>
       <<<ntiles * kc, C::kThreadsTotal, C::kSmemBytes, s>>>(
-          tm, p.npanels, kc, upc, units, part, ov, p.k);
+          tm, p.npanels, kc, upc, units, part, ov);
   return cudaGetLastError();
 }
 
