@@ -167,6 +167,21 @@ int fs_set_gram_engine(int engine);
  * 2 = 8 coalesced 16-B loads in flight per thread (4 KB per warp). */
 int fs_set_pack_engine(int engine);
 
+/* ---- native interactive-recompute loop (service.py:110-175 without the interpreter) ----
+ * A pipeline owns `depth` frame buffers (device outputs, pinned host slots, events) and
+ * `depth` host worker threads.  fs_pipeline_run queues n_frames full recomputes of
+ * slots[0..k) back to back — fused recompute, Jaccard + outlier kernels, D2H of the
+ * [bins | Gram], Jaccard matrix and scores — while the workers run each finished frame's
+ * complete-linkage merge (tau, id_rank as in fs_cluster_complete_linkage).  The last
+ * frame's products go to the (optional) host outputs; *device_ms = device time of the
+ * whole run (CUDA events on the ensemble's compute stream).  Single device.          */
+typedef struct fs_pipeline fs_pipeline;
+int fs_pipeline_create(fs_ensemble *ens, const uint32_t *slots, uint32_t k, int engine, double tau,
+                       const uint32_t *id_rank, uint32_t depth, fs_pipeline **out);
+int fs_pipeline_run(fs_pipeline *p, uint32_t n_frames, int64_t *bins, int64_t *gram, double *sim,
+                    double *scores, int32_t *labels, double *device_ms);
+int fs_pipeline_destroy(fs_pipeline *p);
+
 /* ---- pinned host memory (for zero-staging uploads and fast read-back) ---- */
 int fs_host_alloc(uint64_t bytes, void **out);
 int fs_host_free(void *p);

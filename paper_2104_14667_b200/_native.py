@@ -95,6 +95,10 @@ _SIGNATURES = {
                       C.c_uint64, C.c_uint32, C.c_double, C.c_int],
     "fs_synth_gpu": [_vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
                      C.c_uint64, C.c_uint32, C.c_double],
+    "fs_pipeline_create": [_vp, _u32p, C.c_uint32, C.c_int, C.c_double, _u32p, C.c_uint32,
+                           C.POINTER(_vp)],
+    "fs_pipeline_run": [_vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, C.POINTER(C.c_double)],
+    "fs_pipeline_destroy": [_vp],
 }
 
 EXPORTED_SYMBOLS = ("fs_last_error",) + tuple(_SIGNATURES)

@@ -20,7 +20,7 @@ LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libfloodstream.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["fs_kernels.cu", "fs_gram_tc.cu", "fs_capi.cu"]
+SOURCES = ["fs_kernels.cu", "fs_gram_tc.cu", "fs_capi.cu", "fs_pipeline.cu"]
 HEADERS = ["fs_common.cuh", "fs_internal.h", "fs_bitslice.cuh"]
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -51,6 +51,11 @@ static int cuda_err(cudaError_t e, const char *what) {
     return set_err(FS_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
   return set_err(FS_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+namespace fs {
+// shared with the other C-ABI translation units (fs_pipeline.cu)
+int set_error(int code, const std::string &msg) { return set_err(code, msg); }
+}  // namespace fs
+
 #define CK(call)                                   \
   do {                                             \
     cudaError_t _e = (call);                       \

@@ -1,6 +1,7 @@
 // fs_internal.h — launchers shared between the kernel files and the C ABI layer.
 #pragma once
 #include <cstdint>
+#include <string>
 #include <cuda.h>  // CUtensorMap (types only; the encoder is fetched at run time)
 #include <cuda_runtime.h>
 
@@ -105,6 +106,9 @@ cudaError_t launch_synth_raw(uint8_t *dst, const SynthParams &sp, uint64_t mask,
 
 cudaError_t launch_similarity_outliers(const long long *gram, uint32_t n, double *sim,
                                        double *scores, cudaStream_t s);
+
+// thread-local C-ABI error message + status (fs_capi.cu)
+int set_error(int code, const std::string &msg);
 
 // Composite grey LUT in FP64, bit-exact with _kernels_np.py:41-42.
 void build_grey_lut(uint64_t n_inputs, uint8_t *lut, uint64_t entries);

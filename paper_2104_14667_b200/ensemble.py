@@ -272,6 +272,13 @@ class DeviceEnsemble:
                C.byref(fused))
         return c, b, r, g, bool(fused.value)
 
+    def pipeline(self, slots=None, *, tau: float = 0.8, engine: str = "auto", depth: int = 3,
+                 ids=None) -> "NativePipeline":
+        """Native frame loop over ``slots`` (fs_pipeline_*): recompute, device Jaccard /
+        outliers, D2H and host linkage overlapped in C++ (single device)."""
+        return NativePipeline(self, self._slots(slots), tau=tau, engine=engine, depth=depth,
+                              ids=ids)
+
     def recompute(self, slots=None, *, tau: float = 0.8, engine: str = "auto",
                   overlap: bool = True, pairwise: bool = True) -> Snapshot:
         """Full recompute of the working set: grid, histogram, composite, Gram,
@@ -295,3 +302,61 @@ class DeviceEnsemble:
                 outl = outliers_from_similarity(sim, ids)
             clus = cluster_from_similarity(sim, ids, tau)
         return Snapshot(grid, hist, comp, gram, sim, outl, clus)
+
+
+class NativePipeline:
+    """``depth`` frames in flight, C++ worker threads for the complete-linkage merge
+    (include/floodstream.h, fs_pipeline_*).  ``run(n)`` returns the last frame's products."""
+
+    def __init__(self, ens: DeviceEnsemble, slots: np.ndarray, *, tau: float, engine: str,
+                 depth: int, ids=None):
+        self.ens = ens
+        self.slots = np.ascontiguousarray(slots, dtype=np.uint32)
+        self.k = int(self.slots.size)
+        self.ids = list(ids) if ids is not None else [
+            ens.ids[i] if ens.ids[i] is not None else f"slot{i}" for i in self.slots.tolist()]
+        order = {s: r for r, s in enumerate(sorted(set(self.ids)))}
+        self.rank = np.array([order[s] for s in self.ids], dtype=np.uint32)
+        if not (0.0 < tau <= 1.0):
+            raise ValueError("tau must be in (0, 1]")
+        self.tau = float(tau)
+        h = C.c_void_p()
+        N.call("fs_pipeline_create", ens.handle, self.slots.ctypes.data_as(N._u32p), self.k,
+               _GRAM_ENGINES[engine], self.tau, self.rank.ctypes.data_as(N._u32p), int(depth),
+               C.byref(h))
+        self._h = h
+
+    def run(self, n_frames: int) -> dict:
+        k = self.k
+        bins = np.empty(k + 1, np.int64)
+        gram = np.empty((k, k), np.int64)
+        sim = np.empty((k, k), np.float64)
+        scores = np.empty(max(k, 1), np.float64)
+        labels = np.empty(k, np.int32)
+        ms = C.c_double()
+        N.call("fs_pipeline_run", self._h, int(n_frames), N.ptr(bins), N.ptr(gram), N.ptr(sim),
+               N.ptr(scores), N.ptr(labels), C.byref(ms))
+        members: dict[int, list[str]] = {}
+        for i, lab in enumerate(labels.tolist()):
+            members.setdefault(lab, []).append(self.ids[i])
+        clusters = sorted((sorted(m) for m in members.values()), key=lambda c: c[0])
+        outliers = {sid: scores[i] for i, sid in enumerate(self.ids)} if k >= 2 else None
+        return {"bins": bins, "gram": gram, "similarity": sim, "outliers": outliers,
+                "clusters": clusters, "device_ms": ms.value, "frames": int(n_frames)}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            N.load().fs_pipeline_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -598,3 +598,26 @@ def test_randomized_overlap_and_products(seed):
     assert b2.tolist() == O.overlap_counts(once.reshape(-1), k).tolist()
     assert np.array_equal(r2, O.composite(once, k))
     assert np.array_equal(g2, O.gram(cells))
+
+
+@pytest.mark.parametrize("k,h,w", [(20, 97, 300), (300, 33, 64)])
+def test_native_pipeline(k, h, w):
+    """fs_pipeline_*: the native frame loop gives the oracle's histogram, Gram,
+    similarity, outliers and clusters (last frame of several in flight)."""
+    cells = [synth_cells(w, h, i, members=5, eps=0.04) for i in range(k)]
+    ids = [f"m{i:04d}" for i in range(k)]
+    g = O.gram(cells)
+    sim = O.similarity_from_gram(g)
+    counts = O.accumulate(cells, w, h)
+    with DeviceEnsemble(w, h, k) as ens:
+        ens.upload(cells)
+        with ens.pipeline(list(range(k)), ids=ids, depth=3) as pipe:
+            r1 = pipe.run(1)
+            r = pipe.run(9)
+    for res in (r1, r):
+        assert res["bins"].tolist() == O.overlap_counts(counts.reshape(-1), k).tolist()
+        assert np.array_equal(res["gram"], g)
+        assert res["similarity"].tobytes() == sim.tobytes()
+        assert res["clusters"] == O.cluster(sim, ids, 0.8)
+        assert res["outliers"] == O.outlier_scores(sim, ids)
+    assert r["device_ms"] > 0
