@@ -49,6 +49,12 @@ def main():
     t0 = time.perf_counter()
     sh.run_frames(sl, n, keep=False)
     out["run_frames_us_per_frame"] = round((time.perf_counter() - t0) / n * 1e6, 2)
+    with sh.ens.pipeline(sl, depth=3) as pipe:
+        pipe.run(20)
+        t0 = time.perf_counter()
+        r = pipe.run(n)
+        out["native_pipeline_us_per_frame"] = round((time.perf_counter() - t0) / n * 1e6, 2)
+        out["native_pipeline_device_us_per_frame"] = round(r["device_ms"] * 1e3 / n, 2)
     sh.close()
     print(json.dumps(out))
 
