@@ -673,6 +673,22 @@ def main():
                     "kind::mxf4 reads both operands from SMEM (no TMEM-A form)"}
     dominant = rl_fused
 
+    # ---- the same frames through the native C++ loop (single device, informational) ----
+    native = None
+    if world == 1:
+        with ens.pipeline(slots, tau=args.tau, engine=args.engine, ids=ids, depth=depth) as pipe:
+            pipe.run(args.warmup)
+            torch.cuda.synchronize()
+            t0n = time.perf_counter()
+            rn = pipe.run(args.steps)
+            wall_n = time.perf_counter() - t0n
+        native = {"ms_per_step": round(rn["device_ms"] / args.steps, 4),
+                  "fps": round(args.steps / (rn["device_ms"] / 1e3), 3),
+                  "wall_ms_per_step": round(wall_n / args.steps * 1e3, 4),
+                  "clusters": len(rn["clusters"]),
+                  "path": "fs_pipeline_run: recompute + device Jaccard/outliers + D2H queued "
+                          "while C++ workers run the linkage (no Python per frame)"}
+
     # ---- end-to-end through the public API from pinned host rasters --------------------
     e2e = None
     host = h_counts = None
@@ -742,6 +758,7 @@ def main():
             "fps": round(args.steps / t_res, 3),
             "wall_ms_per_step": round(t_wall / args.steps * 1e3, 4),
             "host_linkage_ms": round(statistics.median(host_ms), 4) if host_ms else None,
+            "native_pipeline": native,
             "clusters": n_clusters if host_ms else None,
             "roofline": dominant,
             "kernels": {"recompute": rl_fused, "overlap": rl_over, "gram": rl_gram},
