@@ -647,6 +647,8 @@ def main():
                 "peak": t_peak, "unit": "TFLOP/s",
                 "frac": round(gram_ops / rc_ms / 1e9 / t_peak, 4),
                 "traffic": traffic.get("k_gram_tc_fused") if (fused and npanels_k == 1) else None,
+                # tensor-pipe utilisation of this kernel from the committed ncu capture
+                "ncu": traffic.get("k_gram_tc_fused_ncu") if (fused and npanels_k == 1) else None,
                 "kernel_ms": round(rc_ms, 4), "ops_per_launch": gram_ops,
                 "ops_def": rl_gram["ops_def"], "peak_note": t_kind,
                 "hbm_achieved_gbs": round(ov_bytes / rc_ms / 1e6, 1),
