@@ -177,6 +177,9 @@ __device__ __forceinline__ void expand_row_f4(uint32_t base, uint32_t row, uint3
 
 constexpr uint32_t kSfCol = 448;          // FP4: scale-factor columns [448, 480) of TMEM
 constexpr uint32_t kSfOnes = 0x7F7F7F7Fu; // UE8M0 127 = 2^0 in every byte
+#ifndef FS_EXP_BATCH
+#define FS_EXP_BATCH 2
+#endif
 constexpr uint64_t kF4MaxChunkPx = 1ull << 24;  // f32 sums stay exact below this
 
 template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false, int FD = 4>
@@ -188,11 +191,15 @@ struct Cfg {
   static constexpr int kExtraBytes = FUSE ? (4 * 32 * kTileTb * 4 + 2 * kFuseBins * 4) : 0;
   static constexpr int kBudget = FUSE ? (232448 - 1024 - 256) : kSmemBudget;
   static constexpr int kRegions = DIAG ? 1 : 2;
-  // 8 expander warps when there are >= 256 operand rows (latency hiding: each thread's
+  // expander work item = one 16-B raw chunk of one operand row per K stage (FP4: 2 per
+  // row).  8 expander warps when there are >= 256 items (latency hiding: each thread's
   // loads -> expand -> stores chain is short), else 4
-  static constexpr int kExpWarps = (PANEL * kRegions >= 256) ? 8 : 4;
+  static constexpr int kChunks = FP4 ? 2 : 1;
+  static constexpr int kItems = PANEL * kRegions * kChunks;
+  static constexpr int kExpWarps = (kItems >= 256) ? 8 : 4;
   static constexpr int kExpThreads = 32 * kExpWarps;
-  static constexpr int kRowsPerThread = PANEL * kRegions / kExpThreads;  // all regions
+  static constexpr int kItemsPerThread = kItems / kExpThreads;
+  static_assert(kItems % kExpThreads == 0, "expander items must split evenly");
   static constexpr int kTmaWarp = kExpWarps + 1;
   static constexpr int kCntWarp0 = kExpWarps + 2;
   static constexpr int kThreadsTotal = 32 * (kExpWarps + 2 + (FUSE ? 4 : 0));
@@ -205,6 +212,10 @@ struct Cfg {
   static constexpr int kStagesFit =
       (kBudget - kDepth * kRawUnitBytes - kExtraBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  // expanders fill kBatch operand stages per pass with one proxy fence: the fence waits
+  // for the pass's shared stores to drain, so batching halves those waits when the
+  // operand ring is deep enough to keep the MMA fed (PANEL 128: 8 stages)
+  static constexpr int kBatch = (kStages >= 6 && kStagesPerUnit % 2 == 0) ? FS_EXP_BATCH : 1;
   static constexpr int kHalves = PANEL / 128;
   static constexpr uint32_t kTmemCols = (PANEL == 256 || FP4) ? 512u : 128u;
   static_assert(!FP4 || DIAG, "FP4 path is for diagonal tiles (off-diagonal accumulators fill TMEM)");
@@ -412,52 +423,58 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
   } else {
     // ===== expanders: raw bits (swizzled) -> 0/1 bytes in SW128 K-major operand =====
     const uint32_t ptid = (uint32_t)(tid - 32);
-    for (int j = 0; j < nst; ++j) {
+    constexpr int kB = C::kBatch;  // stages per pass (never straddles a raw unit)
+    for (int j = 0; j < nst; j += kB) {
       const int u = j / C::kStagesPerUnit;
-      const int sub = j % C::kStagesPerUnit;
+      const int sub0 = j % C::kStagesPerUnit;
       const int ru = u % kRawDepth;
-      const int s = j % C::kStages;
-      if (sub == 0) ptx::mbar_wait(&raw_full[ru], (uint32_t)((u / kRawDepth) & 1));
-      if (j >= C::kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / C::kStages) - 1) & 1));
-      const uint32_t sbase = op_base + s * C::kStageBytes;
+      if (sub0 == 0) ptx::mbar_wait(&raw_full[ru], (uint32_t)((u / kRawDepth) & 1));
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int jj = j + b;
+        if (jj >= C::kStages)
+          ptx::mbar_wait(&empty[jj % C::kStages], (uint32_t)(((jj / C::kStages) - 1) & 1));
+      }
       const uint32_t rbase = raw_base + ru * C::kRawUnitBytes;
-      // all raw loads of this stage first, then the expansion stores: the shared-memory
+      // all raw loads of the pass first, then the expansion stores: the shared-memory
       // accesses are volatile asm (ordered), so interleaving them would serialise every
       // load's latency behind the previous row's stores
-      constexpr int kPer = FP4 ? 2 : 1;  // raw 16-B chunks per row per stage
-      uint4 v[C::kRowsPerThread * kPer];
+      // item i: row (i % rows) of all regions, raw chunk (i / rows); thread ptid takes
+      // items ptid, ptid + kExpThreads, ... (PANEL 256: both chunks of one row)
+      constexpr int kRows = PANEL * C::kRegions;
+      uint4 v[kB][C::kItemsPerThread];
 #pragma unroll
-      for (int m = 0; m < C::kRowsPerThread; ++m) {
-        const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
-        const uint32_t r = idx / PANEL, rr = idx % PANEL;
-        const uint32_t sw = C::kRawRow == 128 ? (rr & 7u) : ((rr >> 1) & 3u);
-        const uint32_t rrow = rbase + r * PANEL * C::kRawRow + rr * C::kRawRow;
-        if (FP4) {
+      for (int b = 0; b < kB; ++b) {
+        const int sub = sub0 + b;
 #pragma unroll
-          for (int hch = 0; hch < 2; ++hch) {
-            const uint32_t u = (uint32_t)(2 * sub + hch);
-            v[m * kPer + hch] = ld_shared_v4(rrow + ((u ^ sw) << 4));
-          }
-        } else {
-          v[m] = ld_shared_v4(rrow + (((uint32_t)sub ^ sw) << 4));
+        for (int m = 0; m < C::kItemsPerThread; ++m) {
+          const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
+          const uint32_t row = idx % kRows, hch = idx / kRows;
+          const uint32_t r = row / PANEL, rr = row % PANEL;
+          const uint32_t sw = C::kRawRow == 128 ? (rr & 7u) : ((rr >> 1) & 3u);
+          const uint32_t rrow = rbase + r * PANEL * C::kRawRow + rr * C::kRawRow;
+          const uint32_t c = FP4 ? (uint32_t)(2 * sub) + hch : (uint32_t)sub;
+          v[b][m] = ld_shared_v4(rrow + ((c ^ sw) << 4));
         }
       }
 #pragma unroll
-      for (int m = 0; m < C::kRowsPerThread; ++m) {
-        const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
-        const uint32_t r = idx / PANEL, rr = idx % PANEL;
-        if (FP4) {
-          // 32 raw bytes (256 px) -> the whole 128-B operand row
+      for (int b = 0; b < kB; ++b) {
+        const uint32_t sbase = op_base + ((j + b) % C::kStages) * C::kStageBytes;
 #pragma unroll
-          for (int hch = 0; hch < 2; ++hch)
-            expand_row_f4(sbase + r * C::kRegionBytes, rr, 4u * hch, v[m * kPer + hch]);
-        } else {
-          expand_row(sbase + r * C::kRegionBytes, rr, v[m]);
+        for (int m = 0; m < C::kItemsPerThread; ++m) {
+          const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
+          const uint32_t row = idx % kRows, hch = idx / kRows;
+          const uint32_t r = row / PANEL, rr = row % PANEL;
+          if (FP4)  // 16 raw bytes (128 px) -> half of the 128-B operand row
+            expand_row_f4(sbase + r * C::kRegionBytes, rr, 4u * hch, v[b][m]);
+          else
+            expand_row(sbase + r * C::kRegionBytes, rr, v[b][m]);
         }
       }
       ptx::fence_proxy_async_smem();
-      ptx::mbar_arrive(&full[s]);
-      if (sub == C::kStagesPerUnit - 1) ptx::mbar_arrive(&raw_empty[ru]);
+#pragma unroll
+      for (int b = 0; b < kB; ++b) ptx::mbar_arrive(&full[(j + b) % C::kStages]);
+      if (sub0 + kB == C::kStagesPerUnit) ptx::mbar_arrive(&raw_empty[ru]);
     }
     // ===== epilogue: TMEM -> registers -> int32 partial tile =====
     const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp

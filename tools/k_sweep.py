@@ -17,7 +17,14 @@ sys.path.insert(0, str(REPO))
 
 
 def main():
+    import argparse
+
     import torch
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", default="", help="k:w:h,... (default: the built-in list)")
+    ap.add_argument("--fused-only", action="store_true", help="skip the separate-pass timings")
+    args = ap.parse_args()
 
     from paper_2104_14667_b200 import _native as N
     from paper_2104_14667_b200.ensemble import DeviceEnsemble
@@ -31,6 +38,8 @@ def main():
     cases = [(16, 1024, 1024), (64, 4096, 4096), (128, 8192, 8192), (256, 8192, 8192),
              (384, 8192, 5461), (512, 8192, 4096), (1024, 4096, 4096), (2048, 4096, 2048),
              (4096, 4096, 1024)]
+    if args.cases:
+        cases = [tuple(int(x) for x in c.split(":")) for c in args.cases.split(",")]
     for k, w, h in cases:
         P = w * h
         with DeviceEnsemble(w, h, k) as ens:
@@ -49,7 +58,7 @@ def main():
             t = statistics.median(ms)
             # the same products as separate passes: overlap kernel + Gram (tc-f4 / popc)
             alt = {}
-            for eng in ("tc-f4", "popc"):
+            for eng in () if args.fused_only else ("tc-f4", "popc"):
                 ov, gr = [], []
                 for it in range(5):
                     ens.overlap(list(range(k)), out_counts=d_c.data_ptr(), out_rgba=d_r.data_ptr(),
