@@ -236,7 +236,7 @@ template <int PANEL, bool DIAG, bool FP4, bool FUSE, int FD>
 __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal, 1)
     k_gram_tc(const __grid_constant__ CUtensorMap tm, uint32_t npanels, uint32_t kchunks,
               uint64_t units_per_chunk, uint64_t total_units, int32_t *__restrict__ partial,
-              const OverlapArgs ov) {
+              const OverlapArgs ov, uint32_t kmasks) {
   using C = Cfg<PANEL, DIAG, FP4, FUSE, FD>;
   constexpr int kRawDepth = C::kDepth;
   extern __shared__ uint8_t smem_raw[];
@@ -279,6 +279,13 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
   const uint64_t u1 = min(u0 + units_per_chunk, total_units);
   const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
   const int nst = nunits * C::kStagesPerUnit;
+  // a single 128-mask panel holding k < 128 masks: MMA N, expanded operand rows and
+  // counted rows shrink to n16 = roundup(k, 16).  Rows >= k of the raw tiles are TMA
+  // out-of-bounds zeros; operand rows >= n16 are never written and only feed
+  // accumulator rows / columns >= k, which k_gram_reduce never reads.
+  constexpr bool kNarrow = PANEL == 128 && FP4 && DIAG;
+  const uint32_t kin = kmasks > I * PANEL ? kmasks - I * PANEL : 0u;
+  const uint32_t n16 = kNarrow ? (kin >= 128u ? 128u : ((kin + 15u) & ~15u)) : (uint32_t)PANEL;
 
   if (tid == 0) {
     ptx::prefetch_tmap(&tm);
@@ -326,30 +333,36 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
   if (warp == 0) {
     // ===== MMA issuer =====
     if (lane == 0 && nst > 0) {
-      constexpr uint32_t idA = FP4 ? idesc_mxf4(128, PANEL) : idesc_i8(128, PANEL);
+      const uint32_t idA = kNarrow ? idesc_mxf4(128, (int)(n16 > 0 ? n16 : 16))
+                           : (FP4 ? idesc_mxf4(128, PANEL) : idesc_i8(128, PANEL));
       constexpr uint32_t idB = FP4 ? idesc_mxf4(128, 128) : idesc_i8(128, 128);
       const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 16;
+      // descriptors = the stage-0 descriptor + byte offset / 16 (the 14-bit start field
+      // never carries below 256 KB): one add per MMA keeps the lone issuing thread's
+      // dependent chain short — at small N the issue loop, not the tensor pipe, sets the
+      // pace (tools/probes/mma_probe.cu)
+      const uint64_t d_op = sw128_desc(op_base);
       for (int j = 0; j < nst; ++j) {
         const int s = j % C::kStages;
         ptx::mbar_wait(&full[s], (uint32_t)((j / C::kStages) & 1));
         fence_after();
-        const uint32_t a_base = op_base + s * C::kStageBytes;
-        const uint32_t b_base = DIAG ? a_base : a_base + C::kRegionBytes;
+        const uint64_t d_a = d_op + (uint64_t)((uint32_t)(s * C::kStageBytes) >> 4);
+        const uint64_t d_b = DIAG ? d_a : d_a + (uint64_t)(C::kRegionBytes >> 4);
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {  // 4 MMAs of 32 B of K per 128-B operand row
           const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
 #pragma unroll
           for (int h = 0; h < C::kHalves; ++h) {
-            const uint64_t adesc = sw128_desc(a_base + h * 128 * 128 + ks * 32);
+            const uint64_t adesc = d_a + (uint64_t)((h * 128 * 128 + ks * 32) >> 4);
             if (DIAG && PANEL == 256 && h == 1) {
               // rows 128..255 x cols 128..255 only
-              const uint64_t bdesc = sw128_desc(b_base + 128 * 128 + ks * 32);
+              const uint64_t bdesc = d_b + (uint64_t)((128 * 128 + ks * 32) >> 4);
               if (FP4)
                 mma_mxf4(tmem + 256u, adesc, bdesc, idB, acc, sfa, sfb);
               else
                 mma_i8(tmem + 256u, adesc, bdesc, idB, acc);
             } else {
-              const uint64_t bdesc = sw128_desc(b_base + ks * 32);
+              const uint64_t bdesc = d_b + (uint64_t)((ks * 32) >> 4);
               if (FP4)
                 mma_mxf4(tmem + (uint32_t)(h * PANEL), adesc, bdesc, idA, acc, sfa, sfb);
               else
@@ -398,7 +411,7 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
       HSCounter<5> hc;
       hc.reset();
 #pragma unroll 1
-      for (int g16 = 0; g16 < PANEL / 16; ++g16) {
+      for (int g16 = 0; g16 < (int)(n16 / 16); ++g16) {
         uint32_t d[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -424,6 +437,20 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
     // ===== expanders: raw bits (swizzled) -> 0/1 bytes in SW128 K-major operand =====
     const uint32_t ptid = (uint32_t)(tid - 32);
     constexpr int kB = C::kBatch;  // stages per pass (never straddles a raw unit)
+    // item i: row (i % rows) of all regions, raw chunk (i / rows); thread ptid takes
+    // items ptid, ptid + kExpThreads, ... (PANEL 256: both chunks of one row)
+    const uint32_t rows_rt = kNarrow ? n16 : (uint32_t)(PANEL * C::kRegions);
+    uint32_t it_r[C::kItemsPerThread], it_rr[C::kItemsPerThread], it_h[C::kItemsPerThread];
+    bool it_on[C::kItemsPerThread];
+#pragma unroll
+    for (int m = 0; m < C::kItemsPerThread; ++m) {
+      const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
+      const uint32_t row = kNarrow ? (rows_rt ? idx % rows_rt : 0u) : idx % (PANEL * C::kRegions);
+      it_h[m] = kNarrow ? (rows_rt ? idx / rows_rt : 0u) : idx / (PANEL * C::kRegions);
+      it_r[m] = row / PANEL;
+      it_rr[m] = row % PANEL;
+      it_on[m] = !kNarrow || idx < rows_rt * C::kChunks;
+    }
     for (int j = 0; j < nst; j += kB) {
       const int u = j / C::kStagesPerUnit;
       const int sub0 = j % C::kStagesPerUnit;
@@ -439,21 +466,17 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
       // all raw loads of the pass first, then the expansion stores: the shared-memory
       // accesses are volatile asm (ordered), so interleaving them would serialise every
       // load's latency behind the previous row's stores
-      // item i: row (i % rows) of all regions, raw chunk (i / rows); thread ptid takes
-      // items ptid, ptid + kExpThreads, ... (PANEL 256: both chunks of one row)
-      constexpr int kRows = PANEL * C::kRegions;
       uint4 v[kB][C::kItemsPerThread];
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
         const int sub = sub0 + b;
 #pragma unroll
         for (int m = 0; m < C::kItemsPerThread; ++m) {
-          const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
-          const uint32_t row = idx % kRows, hch = idx / kRows;
-          const uint32_t r = row / PANEL, rr = row % PANEL;
+          if (!it_on[m]) continue;
+          const uint32_t rr = it_rr[m];
           const uint32_t sw = C::kRawRow == 128 ? (rr & 7u) : ((rr >> 1) & 3u);
-          const uint32_t rrow = rbase + r * PANEL * C::kRawRow + rr * C::kRawRow;
-          const uint32_t c = FP4 ? (uint32_t)(2 * sub) + hch : (uint32_t)sub;
+          const uint32_t rrow = rbase + it_r[m] * PANEL * C::kRawRow + rr * C::kRawRow;
+          const uint32_t c = FP4 ? (uint32_t)(2 * sub) + it_h[m] : (uint32_t)sub;
           v[b][m] = ld_shared_v4(rrow + ((c ^ sw) << 4));
         }
       }
@@ -462,13 +485,11 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
         const uint32_t sbase = op_base + ((j + b) % C::kStages) * C::kStageBytes;
 #pragma unroll
         for (int m = 0; m < C::kItemsPerThread; ++m) {
-          const uint32_t idx = ptid + (uint32_t)m * C::kExpThreads;
-          const uint32_t row = idx % kRows, hch = idx / kRows;
-          const uint32_t r = row / PANEL, rr = row % PANEL;
+          if (!it_on[m]) continue;
           if (FP4)  // 16 raw bytes (128 px) -> half of the 128-B operand row
-            expand_row_f4(sbase + r * C::kRegionBytes, rr, 4u * hch, v[b][m]);
+            expand_row_f4(sbase + it_r[m] * C::kRegionBytes, it_rr[m], 4u * it_h[m], v[b][m]);
           else
-            expand_row(sbase + r * C::kRegionBytes, rr, v[b][m]);
+            expand_row(sbase + it_r[m] * C::kRegionBytes, it_rr[m], v[b][m]);
         }
       }
       ptx::fence_proxy_async_smem();
@@ -490,7 +511,7 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
       const uint32_t row = h * 128 + q * 32 + lane;
       const bool lower_diag = DIAG && PANEL == 256 && h == 1;
       const int c_begin = lower_diag ? 128 : 0;
-      for (int c0 = c_begin + 32 * cg; c0 < PANEL; c0 += 32 * kColGroups) {
+      for (int c0 = c_begin + 32 * cg; c0 < (int)n16; c0 += 32 * kColGroups) {
         uint32_t v[32];
         const uint32_t col =
             lower_diag ? (256u + (uint32_t)(c0 - 128)) : (uint32_t)(h * PANEL + c0);
@@ -674,15 +695,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     if (rank == 0 && lane == 0 && nst > 0) {
       constexpr uint32_t idesc = idesc_mxf4(256, 256);
       const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 16;
+      const uint64_t d_op = sw128_desc(op_base);  // + byte offset / 16, as in k_gram_tc
       for (int j = 0; j < nst; ++j) {
         const int s = j % kPairStages;
         mbar_wait_cluster(&full[s], (uint32_t)((j / kPairStages) & 1));
         fence_after();
-        const uint32_t a_base = op_base + s * kPairStageBytes;
-        const uint32_t b_base = a_base + 128 * 128;
+        const uint64_t d_a = d_op + (uint64_t)((uint32_t)(s * kPairStageBytes) >> 4);
+        const uint64_t d_b = d_a + (uint64_t)((128 * 128) >> 4);
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
-          mma_mxf4_pair(tmem, sw128_desc(a_base + ks * 32), sw128_desc(b_base + ks * 32), idesc,
+          mma_mxf4_pair(tmem, d_a + (uint64_t)(ks * 2), d_b + (uint64_t)(ks * 2), idesc,
                         (j > 0 || ks > 0) ? 1u : 0u, sfa, sfb);
         mma_commit_pair(&empty[s]);
       }
@@ -821,6 +843,7 @@ __global__ void k_gather_slots(const uint32_t *__restrict__ packed, uint64_t cap
 
 struct Plan {
   int panel;
+  uint32_t k;  // masks
   bool pair;  // off-diagonal tiles on CTA pairs (kind::mxf4, cta_group::2)
   uint32_t npanels, ndiag, noff;
   uint64_t units_diag, units_off;  // raw units along K for each tile kind
@@ -866,6 +889,7 @@ static void chunking(uint64_t total_units, uint32_t ntiles, int slots, uint32_t 
 
 static Plan make_plan(uint32_t k, uint64_t wpm, int num_sms, bool fp4) {
   Plan p{};
+  p.k = k;
   p.panel = k <= 128 ? 128 : 256;
   p.npanels = (k + p.panel - 1) / p.panel;
   p.ndiag = p.npanels;
@@ -923,7 +947,7 @@ static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t 
   }
   tc::k_gram_tc<PANEL, DIAG, FP4, FUSE, FD>
       <<<ntiles * kc, C::kThreadsTotal, C::kSmemBytes, s>>>(
-          tm, p.npanels, kc, upc, units, part, ov);
+          tm, p.npanels, kc, upc, units, part, ov, p.k);
   return cudaGetLastError();
 }
 
