@@ -60,6 +60,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         "-I",
         str(CSRC),
         *(["-Xptxas", "-v"] if verbose else []),
+        # experiment knobs (e.g. -DFS_EXP_BATCH=1); never set for the shipped build
+        *os.environ.get("FS_NVCC_EXTRA", "").split(),
         *[str(CSRC / s) for s in SOURCES],
         "-o",
         str(tmp),

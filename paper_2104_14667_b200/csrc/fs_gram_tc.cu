@@ -177,6 +177,15 @@ __device__ __forceinline__ void expand_row_f4(uint32_t base, uint32_t row, uint3
 
 constexpr uint32_t kSfCol = 448;          // FP4: scale-factor columns [448, 480) of TMEM
 constexpr uint32_t kSfOnes = 0x7F7F7F7Fu; // UE8M0 127 = 2^0 in every byte
+// 256-mask fused diagonal: raw ring depth (= counter warps up to 4).  4 x 32 KB raw
+// units leave room for 2 operand stages.  Depth 2 (2 counter warps, 4 operand stages)
+// measured slower, 1.41 vs 1.08 ms at C2: two counter warps cannot keep up
+// (profiles/r3f/parts.txt)
+#ifndef FS_FUSE_DEPTH_256
+#define FS_FUSE_DEPTH_256 4
+#endif
+constexpr int kFuseDepth256 = FS_FUSE_DEPTH_256;
+
 #ifndef FS_EXP_BATCH
 #define FS_EXP_BATCH 2
 #endif
@@ -184,11 +193,14 @@ constexpr uint64_t kF4MaxChunkPx = 1ull << 24;  // f32 sums stay exact below thi
 
 template <int PANEL, bool DIAG, bool FP4 = false, bool FUSE = false, int FD = 4>
 struct Cfg {
-  // raw ring depth.  FUSE: 4 = one slot per counter warp (unit u lives in slot u % 4 and
-  // is counted by warp u % 4), so a counter warp only ever waits on its own slot, in
-  // order, and can never run a full mbarrier phase ahead of it.
+  // raw ring depth.  FUSE: a multiple of the counter-warp count (unit u lives in slot
+  // u % kDepth and is counted by warp u % kCntWarps), so a counter warp only ever waits
+  // on its own slots, in order, and can never run a full mbarrier phase ahead of them.
   static constexpr int kDepth = FUSE ? FD : kRawDepth;
-  static constexpr int kExtraBytes = FUSE ? (4 * 32 * kTileTb * 4 + 2 * kFuseBins * 4) : 0;
+  // FUSE: counter warps; warp cw counts units cw, cw + kCntWarps, ... (FD = raw ring depth)
+  static constexpr int kCntWarps = FUSE ? (FD < 4 ? FD : 4) : 0;
+  static constexpr int kExtraBytes =
+      FUSE ? (kCntWarps * 32 * kTileTb * 4 + 2 * kFuseBins * 4) : 0;
   static constexpr int kBudget = FUSE ? (232448 - 1024 - 256) : kSmemBudget;
   static constexpr int kRegions = DIAG ? 1 : 2;
   // expander work item = one 16-B raw chunk of one operand row per K stage (FP4: 2 per
@@ -202,7 +214,7 @@ struct Cfg {
   static_assert(kItems % kExpThreads == 0, "expander items must split evenly");
   static constexpr int kTmaWarp = kExpWarps + 1;
   static constexpr int kCntWarp0 = kExpWarps + 2;
-  static constexpr int kThreadsTotal = 32 * (kExpWarps + 2 + (FUSE ? 4 : 0));
+  static constexpr int kThreadsTotal = 32 * (kExpWarps + 2 + kCntWarps);
   static constexpr int kRawRow = (PANEL == 256 && !DIAG) ? 64 : 128;  // raw bytes/row/unit
   static constexpr int kRawPerStage = FP4 ? 32 : 16;  // raw bytes per row per K stage
   static constexpr int kStagesPerUnit = kRawRow / kRawPerStage;
@@ -220,13 +232,14 @@ struct Cfg {
   static constexpr uint32_t kTmemCols = (PANEL == 256 || FP4) ? 512u : 128u;
   static_assert(!FP4 || DIAG, "FP4 path is for diagonal tiles (off-diagonal accumulators fill TMEM)");
   static_assert(!FUSE || DIAG, "the fused overlap pass runs in diagonal tiles");
-  // FUSE: counter warp u % 4 takes unit u from slot u % kDepth.  With kDepth a
-  // multiple of 4 the previous occupant of that slot (unit u - kDepth) was counted by
-  // the same warp, so when the warp waits for unit u the slot holds u - kDepth or u and
-  // the phase parity tells them apart.  With fewer slots the previous occupant belongs
-  // to another warp, the expanders may still hold the slot two phases back, and the
-  // parity wait would pass on stale data (caught by the parity tests at depth 2 and 3).
-  static_assert(!FUSE || kDepth % 4 == 0, "counter warp u % 4 must own slot u % kDepth");
+  // FUSE: counter warp u % kCntWarps takes unit u from slot u % kDepth.  With kDepth a
+  // multiple of kCntWarps the previous occupant of that slot (unit u - kDepth) was
+  // counted by the same warp, so when the warp waits for unit u the slot holds
+  // u - kDepth or u and the phase parity tells them apart.  Otherwise the previous
+  // occupant belongs to another warp, the expanders may still hold the slot two phases
+  // back, and the parity wait would pass on stale data (the parity tests caught it with
+  // 4 counter warps at depth 2 and 3).
+  static_assert(!FUSE || kDepth % kCntWarps == 0, "counter warp u % kCntWarps must own slot u % kDepth");
   static constexpr int kSmemBytes = kDepth * kRawUnitBytes + kStages * kStageBytes + kExtraBytes +
                                     1024 /*align*/ + 256 /*barriers*/;
   static_assert(kStages >= 2, "operand ring too shallow");
@@ -248,7 +261,7 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
   const uint32_t op_base = smem_base + kRawDepth * C::kRawUnitBytes;    // operand stages
   uint8_t *extra = smem + kRawDepth * C::kRawUnitBytes + C::kStages * C::kStageBytes;
   uint32_t *cnt_tb = reinterpret_cast<uint32_t *>(extra);        // FUSE: 4 x 32 x kTileTb
-  uint32_t *sh_hist = cnt_tb + 4 * 32 * kTileTb;                 // FUSE: kFuseBins
+  uint32_t *sh_hist = cnt_tb + C::kCntWarps * 32 * kTileTb;      // FUSE: kFuseBins
   uint32_t *sh_lut = sh_hist + kFuseBins;                        // FUSE: kFuseBins
   uint64_t *full = reinterpret_cast<uint64_t *>(extra + C::kExtraBytes);
   uint64_t *empty = full + C::kStages;
@@ -290,19 +303,19 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
   if (tid == 0) {
     ptx::prefetch_tmap(&tm);
     for (int s = 0; s < C::kStages; ++s) {
-      ptx::mbar_init(&full[s], C::kExpThreads);
+      ptx::mbar_init(&full[s], C::kExpWarps);  // one arrive per expander warp
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kRawDepth; ++s) {
       ptx::mbar_init(&raw_full[s], 1);
-      ptx::mbar_init(&raw_empty[s], FUSE ? C::kExpThreads + 32 : C::kExpThreads);
+      ptx::mbar_init(&raw_empty[s], FUSE ? C::kExpWarps + 1 : C::kExpWarps);
     }
     ptx::mbar_init(tmem_full, 1);
     ptx::fence_mbar_init();
   }
   const bool lut_sh = FUSE && ov.rgba != nullptr;
   if (FUSE && warp >= C::kCntWarp0) {
-    for (int i = tid - 32 * C::kCntWarp0; i < kFuseBins; i += 128) {
+    for (int i = tid - 32 * C::kCntWarp0; i < kFuseBins; i += 32 * C::kCntWarps) {
       sh_hist[i] = 0;
       sh_lut[i] = lut_sh && (uint32_t)i < ov.nbins ? rgba_word(i, ov.n_inputs, ov.lut) : 0u;
     }
@@ -363,10 +376,12 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
                 mma_i8(tmem + 256u, adesc, bdesc, idB, acc);
             } else {
               const uint64_t bdesc = d_b + (uint64_t)((ks * 32) >> 4);
+#ifndef FS_PROBE_NO_MMA  // timing experiment only: the kernel without its main MMAs
               if (FP4)
                 mma_mxf4(tmem + (uint32_t)(h * PANEL), adesc, bdesc, idA, acc, sfa, sfb);
               else
                 mma_i8(tmem + (uint32_t)(h * PANEL), adesc, bdesc, idA, acc);
+#endif
             }
           }
         }
@@ -404,10 +419,15 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       off[j] = ((((uint32_t)lane >> 2) ^ (uint32_t)j) << 4) + ((uint32_t)lane & 3u) * 4u;
-    for (int u = cw; u < nunits; u += 4) {
+    for (int u = cw; u < nunits; u += C::kCntWarps) {
       const int ru = u % kRawDepth;
       ptx::mbar_wait(&raw_full[ru], (uint32_t)((u / kRawDepth) & 1));
       const uint32_t rb = raw_base + ru * C::kRawUnitBytes;
+#ifdef FS_PROBE_NO_COUNT  // timing experiment only
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&raw_empty[ru]);
+      continue;
+#endif
       HSCounter<5> hc;
       hc.reset();
 #pragma unroll 1
@@ -421,11 +441,15 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
         hc.add16(d);
       }
       __syncwarp();
-      ptx::mbar_arrive(&raw_empty[ru]);
+      if (lane == 0) ptx::mbar_arrive(&raw_empty[ru]);
       uint32_t cnt32[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) cnt32[j] = 0;
       hc.extract(cnt32, 1u);
+#ifdef FS_PROBE_NO_EMIT  // timing experiment only
+      if (cnt32[lane & 31] == 0xFFFFFFFFu) ov.counts[0] = 0;  // keep the count live
+      continue;
+#endif
       if (ov.partial16 != nullptr)  // multi-panel: this panel's counts, summed later
         emit_partial16(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb,
                        ov.partial16 + (uint64_t)I * ov.part_pitch);
@@ -467,6 +491,7 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
       // accesses are volatile asm (ordered), so interleaving them would serialise every
       // load's latency behind the previous row's stores
       uint4 v[kB][C::kItemsPerThread];
+#ifndef FS_PROBE_NO_EXPAND  // timing experiment only: skip the expansion work
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
         const int sub = sub0 + b;
@@ -492,10 +517,17 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
             expand_row(sbase + it_r[m] * C::kRegionBytes, it_rr[m], v[b][m]);
         }
       }
+#endif
+      // every writer fences its own stores into the async proxy; after the warp
+      // converges one lane arrives for the warp (kExpWarps arrivals per barrier phase
+      // instead of one per thread: 256 same-word arrives serialised the handoff)
       ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
 #pragma unroll
-      for (int b = 0; b < kB; ++b) ptx::mbar_arrive(&full[(j + b) % C::kStages]);
-      if (sub0 + kB == C::kStagesPerUnit) ptx::mbar_arrive(&raw_empty[ru]);
+        for (int b = 0; b < kB; ++b) ptx::mbar_arrive(&full[(j + b) % C::kStages]);
+        if (sub0 + kB == C::kStagesPerUnit) ptx::mbar_arrive(&raw_empty[ru]);
+      }
     }
     // ===== epilogue: TMEM -> registers -> int32 partial tile =====
     const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp
@@ -533,7 +565,7 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
   }
   __syncthreads();
   if (FUSE && warp >= C::kCntWarp0 && ov.bins != nullptr) {
-    for (uint32_t i = tid - 32 * C::kCntWarp0; i < ov.nbins; i += 128)
+    for (uint32_t i = tid - 32 * C::kCntWarp0; i < ov.nbins; i += 32 * C::kCntWarps)
       if (sh_hist[i]) atomicAdd(ov.bins + i, (unsigned long long)sh_hist[i]);
     if (blockIdx.x == 0 && tid == 32 * C::kCntWarp0) {
       const uint64_t pad = total_units * 1024 - ov.pixels;  // padding counted in bin 0
@@ -1025,10 +1057,10 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
     if ((e = launch_one<128, false>(tm_off, p, part_off, none, s)) != cudaSuccess) return e;
   } else {
     if (fuse_now)
-      e = fp4 ? launch_one<256, true, true, true>(tm_diag, p, part_diag, *fuse, s)
+      e = fp4 ? launch_one<256, true, true, true, tc::kFuseDepth256>(tm_diag, p, part_diag, *fuse, s)
               : launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s);
     else if (fuse_multi)
-      e = launch_one<256, true, true, true>(tm_diag, p, part_diag, ovp, s);
+      e = launch_one<256, true, true, true, tc::kFuseDepth256>(tm_diag, p, part_diag, ovp, s);
     else
       e = fp4 ? launch_one<256, true, true>(tm_diag, p, part_diag, none, s)
               : launch_one<256, true>(tm_diag, p, part_diag, none, s);
