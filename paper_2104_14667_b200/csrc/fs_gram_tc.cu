@@ -385,7 +385,11 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
             }
           }
         }
+#ifdef FS_PROBE_PLAIN_ARRIVE  // timing experiment only (with FS_PROBE_NO_MMA)
+        ptx::mbar_arrive(&empty[s]);
+#else
         mma_commit(&empty[s]);
+#endif
       }
       mma_commit(tmem_full);
     }
@@ -521,7 +525,9 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
       // every writer fences its own stores into the async proxy; after the warp
       // converges one lane arrives for the warp (kExpWarps arrivals per barrier phase
       // instead of one per thread: 256 same-word arrives serialised the handoff)
+#ifndef FS_PROBE_NO_FENCE  // timing experiment only (racy without the fence)
       ptx::fence_proxy_async_smem();
+#endif
       __syncwarp();
       if (lane == 0) {
 #pragma unroll
