@@ -334,7 +334,9 @@ def test_gram_f4_chunk_cap_large_k_range():
 @pytest.mark.parametrize("k,h,w", [(1, 5, 7), (3, 33, 31), (16, 64, 64), (100, 40, 70),
                                    (128, 32, 33), (129, 17, 65), (256, 24, 40),
                                    (257, 16, 33), (300, 9, 130), (64, 1500, 1100),
-                                   (200, 700, 2000), (256, 613, 1999)])
+                                   (200, 700, 2000), (256, 613, 1999),
+                                   # narrow panel (MMA N = roundup(k, 16) < 128), many K chunks
+                                   (33, 1100, 1500), (127, 300, 700)])
 def test_products_match_oracle(engine, k, h, w):
     rng = np.random.default_rng(7 * k + h)
     cells = [(rng.random((h, w)) < rng.uniform(0.05, 0.95)).astype(np.uint8) *
