@@ -447,9 +447,7 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
       __syncwarp();
       ptx::mbar_arrive(&raw_empty[ru]);
       uint32_t cnt32[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) cnt32[j] = 0;
-      hc.extract(cnt32, 1u);
+      hc.extract1(cnt32);
 #ifdef FS_PROBE_NO_EMIT  // timing experiment only
       if (cnt32[lane & 31] == 0xFFFFFFFFu) ov.counts[0] = 0;  // keep the count live
       continue;
