@@ -42,7 +42,7 @@ def main():
     assert np.array_equal(out, want)
     print("primitives ok", flush=True)
 
-    for (w, h, k) in [(130, 33, 20), (64, 40, 300)]:
+    for (w, h, k) in [(130, 33, 20), (96, 20, 256), (64, 40, 300)]:
         cells = [synth_cells(w, h, i, members=5, eps=0.05) for i in range(k)]
         with DeviceEnsemble(w, h, k) as ens:
             ens.stream(cells, variant="2b-final", with_kernel=True)
