@@ -672,7 +672,11 @@ def main():
             "smem_bound_ms": round(smem_ms, 4), "mma_bound_ms": round(mma_ms, 4),
             "frac_of_smem_bound": round(smem_ms / rc_ms, 4),
             "note": "no binary tcgen05 kind: 1-bit masks are expanded to e2m1 in SMEM and "
-                    "kind::mxf4 reads both operands from SMEM (no TMEM-A form)"}
+                    "kind::mxf4 reads both operands from SMEM (no TMEM-A form)",
+            # the kernel rebuilt without each part in turn (FS_PROBE_* builds): skeleton
+            # (TMA ring + stage handoffs) 0.53 ms, + expansion 0.67, + counting 0.87,
+            # + MMAs 1.08 at C2; TMA alone streams the same boxes at 7.25 TB/s
+            "part_isolation": "profiles/r3f/parts.txt"}
     dominant = rl_fused
 
     # ---- the same frames through the native C++ loop (single device, informational) ----
