@@ -477,26 +477,18 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
       it_rr[m] = row % PANEL;
       it_on[m] = !kNarrow || idx < rows_rt * C::kChunks;
     }
-    for (int j = 0; j < nst; j += kB) {
-      const int u = j / C::kStagesPerUnit;
-      const int sub0 = j % C::kStagesPerUnit;
-      const int ru = u % kRawDepth;
-      if (sub0 == 0) ptx::mbar_wait(&raw_full[ru], (uint32_t)((u / kRawDepth) & 1));
+    // raw loads of pass p + 1 are issued right after pass p's operand stores and before
+    // its proxy fence, so the fence's wait for the stores to drain overlaps the next
+    // pass's shared-memory load latency (the accesses are volatile asm, kept in order)
+    auto load_pass = [&](int jp, uint4 (&vv)[kB][C::kItemsPerThread]) {
+      const int up = jp / C::kStagesPerUnit;
+      const int subp = jp % C::kStagesPerUnit;
+      const int rup = up % kRawDepth;
+      if (subp == 0) ptx::mbar_wait(&raw_full[rup], (uint32_t)((up / kRawDepth) & 1));
+      const uint32_t rbase = raw_base + rup * C::kRawUnitBytes;
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
-        const int jj = j + b;
-        if (jj >= C::kStages)
-          ptx::mbar_wait(&empty[jj % C::kStages], (uint32_t)(((jj / C::kStages) - 1) & 1));
-      }
-      const uint32_t rbase = raw_base + ru * C::kRawUnitBytes;
-      // all raw loads of the pass first, then the expansion stores: the shared-memory
-      // accesses are volatile asm (ordered), so interleaving them would serialise every
-      // load's latency behind the previous row's stores
-      uint4 v[kB][C::kItemsPerThread];
-#ifndef FS_PROBE_NO_EXPAND  // timing experiment only: skip the expansion work
-#pragma unroll
-      for (int b = 0; b < kB; ++b) {
-        const int sub = sub0 + b;
+        const int sub = subp + b;
 #pragma unroll
         for (int m = 0; m < C::kItemsPerThread; ++m) {
           if (!it_on[m]) continue;
@@ -504,9 +496,27 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
           const uint32_t sw = C::kRawRow == 128 ? (rr & 7u) : ((rr >> 1) & 3u);
           const uint32_t rrow = rbase + it_r[m] * PANEL * C::kRawRow + rr * C::kRawRow;
           const uint32_t c = FP4 ? (uint32_t)(2 * sub) + it_h[m] : (uint32_t)sub;
-          v[b][m] = ld_shared_v4(rrow + ((c ^ sw) << 4));
+          vv[b][m] = ld_shared_v4(rrow + ((c ^ sw) << 4));
         }
       }
+    };
+    // (one stage per pass only: with two-stage passes, the 128-mask panel, holding the
+    // next pass's loads across the fence measured 2 % slower)
+    constexpr bool kPrefetch = kB == 1;
+    uint4 v[kB][C::kItemsPerThread];
+    if (kPrefetch && nst > 0) load_pass(0, v);
+    for (int j = 0; j < nst; j += kB) {
+      const int u = j / C::kStagesPerUnit;
+      const int sub0 = j % C::kStagesPerUnit;
+      const int ru = u % kRawDepth;
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int jj = j + b;
+        if (jj >= C::kStages)
+          ptx::mbar_wait(&empty[jj % C::kStages], (uint32_t)(((jj / C::kStages) - 1) & 1));
+      }
+      if (!kPrefetch) load_pass(j, v);
+#ifndef FS_PROBE_NO_EXPAND  // timing experiment only: skip the expansion work
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
         const uint32_t sbase = op_base + ((j + b) % C::kStages) * C::kStageBytes;
@@ -520,6 +530,8 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
         }
       }
 #endif
+      uint4 vn[kB][C::kItemsPerThread];
+      if (kPrefetch && j + kB < nst) load_pass(j + kB, vn);
       // every writer fences its own stores into the async proxy and arrives (one
       // arrive per warp after __syncwarp measured 2 % slower at C2: 1.105 vs 1.08 ms)
 #ifndef FS_PROBE_NO_FENCE  // timing experiment only (racy without the fence)
@@ -528,6 +540,12 @@ __global__ void __launch_bounds__(Cfg<PANEL, DIAG, FP4, FUSE, FD>::kThreadsTotal
 #pragma unroll
       for (int b = 0; b < kB; ++b) ptx::mbar_arrive(&full[(j + b) % C::kStages]);
       if (sub0 + kB == C::kStagesPerUnit) ptx::mbar_arrive(&raw_empty[ru]);
+      if (kPrefetch) {
+#pragma unroll
+        for (int b = 0; b < kB; ++b)
+#pragma unroll
+          for (int m = 0; m < C::kItemsPerThread; ++m) v[b][m] = vn[b][m];
+      }
     }
     // ===== epilogue: TMEM -> registers -> int32 partial tile =====
     const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp
