@@ -779,23 +779,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const uint32_t et = (uint32_t)(tid - 32);
     const uint32_t reg = et >> 7, rr = et & 127u;
     const uint32_t sw = rr & 7u;
+    // as in k_gram_tc: the next stage's raw loads go out before this stage's proxy fence
+    // (within a raw unit only — with a 2-deep raw ring, waiting for the next unit before
+    // releasing this one would delay its refill)
+    auto load = [&](int jp, uint4 &a, uint4 &b) {
+      const int up = jp / kSub, subp = jp % kSub;
+      const int rup = up % kPairDepth;
+      if (subp == 0) ptx::mbar_wait(&raw_full[rup], (uint32_t)((up / kPairDepth) & 1));
+      const uint32_t rrow = raw_base + rup * kPairRawUnit + reg * 128 * 128 + rr * 128;
+      a = ld_shared_v4(rrow + ((((uint32_t)(2 * subp)) ^ sw) << 4));
+      b = ld_shared_v4(rrow + ((((uint32_t)(2 * subp + 1)) ^ sw) << 4));
+    };
+    uint4 v0, v1;
+    bool have = false;
     for (int j = 0; j < nst; ++j) {
       const int u = j / kSub, sub = j % kSub;
       const int ru = u % kPairDepth;
       const int s = j % kPairStages;
-      if (sub == 0) ptx::mbar_wait(&raw_full[ru], (uint32_t)((u / kPairDepth) & 1));
+      if (!have) load(j, v0, v1);
       if (j >= kPairStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / kPairStages) - 1) & 1));
-      const uint32_t rrow = raw_base + ru * kPairRawUnit + reg * 128 * 128 + rr * 128;
-      const uint4 v0 = ld_shared_v4(rrow + ((((uint32_t)(2 * sub)) ^ sw) << 4));
-      const uint4 v1 = ld_shared_v4(rrow + ((((uint32_t)(2 * sub + 1)) ^ sw) << 4));
       const uint32_t obase = op_base + s * kPairStageBytes + reg * 128 * 128;
       expand_row_f4(obase, rr, 0u, v0);
       expand_row_f4(obase, rr, 4u, v1);
+      uint4 n0, n1;
+      have = j + 1 < nst && (j + 1) % kSub != 0;
+      if (have) load(j + 1, n0, n1);
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive_cluster(&full[s], 0);
         if (sub == kSub - 1) ptx::mbar_arrive(&raw_empty[ru]);
+      }
+      if (have) {
+        v0 = n0;
+        v1 = n1;
       }
     }
     // ===== epilogue: this CTA's 128 rows x 256 columns of D =====
