@@ -59,8 +59,10 @@ extern "C" {
 #define FS_GRAM_AUTO 0
 #define FS_GRAM_POPC 1   /* CUDA-core AND+POPC on bit-packed masks           */
 #define FS_GRAM_TC_I8 2  /* tcgen05 kind::i8, bits expanded to u8 in SMEM    */
-#define FS_GRAM_TC_F4 3  /* diagonal tiles on tcgen05 kind::mxf4 (e2m1, scale 1, f32 exact
-                            per <= 2^24-px chunk), off-diagonal tiles on kind::i8 */
+#define FS_GRAM_TC_F4 3  /* tcgen05 kind::mxf4 (bits expanded to e2m1 0/1 in SMEM, block
+                            scale 1, f32 exact per <= 2^24-px K chunk): diagonal 256-mask
+                            panels on one CTA each, off-diagonal 256 x 256 tiles on CTA
+                            pairs (cta_group::2, M = 256, N = 256)                 */
 
 /* ---- housekeeping ------------------------------------------------------ */
 const char *fs_last_error(void);
@@ -82,6 +84,14 @@ int fs_composite_fill(const uint32_t *counts, uint64_t n, uint64_t n_inputs, uin
 int fs_accumulate_many(uint32_t *counts, const uint8_t *const *cells, uint32_t k, uint64_t n);
 /* gram[i*k+j] = |wet(cells[i]) & wet(cells[j])| for all i, j (int64, symmetric) */
 int fs_gram_many(const uint8_t *const *cells, uint32_t k, uint64_t n, int64_t *gram);
+/* Both calls above keep the stack bit-packed in HBM, in one cache per device keyed by
+ * a 128-bit fingerprint of each raster's bytes (hashed on host threads per call): a
+ * raster whose content is already resident is not uploaded again, so the drop-in
+ * sequence accumulate -> similarity_matrix -> outlier_scores -> cluster_surfaces
+ * (analytics.py:106-240) uploads the stack once.  Shared by all threads (one lock per
+ * device); at most 4 GiB of packed masks stay cached between calls.                 */
+int fs_stack_cache_release(void);  /* free the calling device's cache */
+int fs_stack_cache_info(uint32_t *slots_valid, uint32_t *capacity, uint64_t *pixels);
 
 /* ---- resident ensemble: bit-packed masks kept in HBM ---------------------- */
 typedef struct fs_ensemble fs_ensemble;

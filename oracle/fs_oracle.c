@@ -88,31 +88,71 @@ int fso_pair_counts(const uint8_t *a, const uint8_t *b, uint64_t n, int64_t *int
   return 0;
 }
 
-/* pack wet bits, then |A_i & A_j| by 64-bit popcounts over all pairs i <= j */
+/* pack wet bits, then |A_i & A_j| by 64-bit popcounts over all pairs i <= j.
+ * Blocked for full-size configs (C2: 256 x 2^26 px, C3: 1024 x 2^24, C4 bands): work
+ * units are (block of BM masks) x (block of BM masks) x (segment of words); a unit sums
+ * its segment in sub-chunks of CW words (both blocks' chunks stay in L2) and adds the
+ * partial counts into the shared Gram atomically.  Same integers as the plain pair loop. */
+#define FSO_BM 16
+#define FSO_CW 512
 int fso_gram(const uint8_t *const *cells, uint32_t k, uint64_t n, int64_t *gram, int threads) {
   const uint64_t words = (n + 63) / 64;
-  uint64_t *bits = (uint64_t *)calloc((size_t)k * words, sizeof(uint64_t));
+  uint64_t *bits = (uint64_t *)malloc((size_t)k * words * sizeof(uint64_t) + 8);
   if (!bits) return 3;
   int T = nthreads(threads);
-#pragma omp parallel for schedule(static) num_threads(T)
-  for (int64_t s = 0; s < (int64_t)k; ++s)
-    for (uint64_t p = 0; p < n; ++p)
-      if (cells[s][p] > 0) bits[(size_t)s * words + p / 64] |= 1ull << (p % 64);
-  const int64_t npairs = (int64_t)k * (k + 1) / 2;
-#pragma omp parallel for schedule(dynamic, 1) num_threads(T)
-  for (int64_t e = 0; e < npairs; ++e) {
-    /* e -> (i, j), i <= j */
-    int64_t i = 0, rem = e;
-    while (rem >= (int64_t)k - i) {
-      rem -= (int64_t)k - i;
-      ++i;
+  const int64_t wblocks = (int64_t)((words + 4095) / 4096);
+#pragma omp parallel for schedule(dynamic, 4) num_threads(T)
+  for (int64_t u = 0; u < (int64_t)k * wblocks; ++u) {
+    const uint64_t s = (uint64_t)(u / wblocks), w0 = (uint64_t)(u % wblocks) * 4096;
+    const uint64_t w1 = w0 + 4096 < words ? w0 + 4096 : words;
+    const uint8_t *c = cells[s];
+    for (uint64_t w = w0; w < w1; ++w) {
+      uint64_t v = 0, p0 = w * 64, p1 = p0 + 64 < n ? p0 + 64 : n;
+      for (uint64_t p = p0; p < p1; ++p) v |= (uint64_t)(c[p] > 0) << (p - p0);
+      bits[s * words + w] = v;
     }
-    int64_t j = i + rem;
-    const uint64_t *x = bits + (size_t)i * words, *y = bits + (size_t)j * words;
-    int64_t s = 0;
-    for (uint64_t w = 0; w < words; ++w) s += __builtin_popcountll(x[w] & y[w]);
-    gram[i * k + j] = s;
-    gram[j * k + i] = s;
+  }
+  memset(gram, 0, (size_t)k * k * sizeof(int64_t));
+  const int64_t nb = ((int64_t)k + FSO_BM - 1) / FSO_BM;
+  const int64_t bpairs = nb * (nb + 1) / 2;
+  /* enough segments that every thread gets several units */
+  int64_t segs = (4 * (int64_t)T + bpairs - 1) / bpairs;
+  if (segs < 1) segs = 1;
+  int64_t seg_words = (int64_t)((words + segs - 1) / segs);
+  seg_words = (seg_words + FSO_CW - 1) / FSO_CW * FSO_CW;
+  if (seg_words < FSO_CW) seg_words = FSO_CW;
+  segs = ((int64_t)words + seg_words - 1) / seg_words;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(T)
+  for (int64_t u = 0; u < bpairs * segs; ++u) {
+    int64_t e = u / segs, sg = u % segs;
+    int64_t bi = 0;
+    while (e >= nb - bi) { e -= nb - bi; ++bi; }
+    const int64_t bj = bi + e;
+    const int64_t i0 = bi * FSO_BM, i1 = i0 + FSO_BM < (int64_t)k ? i0 + FSO_BM : (int64_t)k;
+    const int64_t j0 = bj * FSO_BM, j1 = j0 + FSO_BM < (int64_t)k ? j0 + FSO_BM : (int64_t)k;
+    int64_t acc[FSO_BM][FSO_BM];
+    memset(acc, 0, sizeof(acc));
+    const uint64_t s0 = (uint64_t)sg * (uint64_t)seg_words;
+    const uint64_t s1 = s0 + (uint64_t)seg_words < words ? s0 + (uint64_t)seg_words : words;
+    for (uint64_t c0 = s0; c0 < s1; c0 += FSO_CW) {
+      const uint64_t c1 = c0 + FSO_CW < s1 ? c0 + FSO_CW : s1;
+      for (int64_t i = i0; i < i1; ++i) {
+        const uint64_t *x = bits + (size_t)i * words;
+        for (int64_t j = (bi == bj ? i : j0); j < j1; ++j) {
+          const uint64_t *y = bits + (size_t)j * words;
+          int64_t s = 0;
+          for (uint64_t w = c0; w < c1; ++w) s += __builtin_popcountll(x[w] & y[w]);
+          acc[i - i0][j - j0] += s;
+        }
+      }
+    }
+    for (int64_t i = i0; i < i1; ++i)
+      for (int64_t j = (bi == bj ? i : j0); j < j1; ++j) {
+        const int64_t s = acc[i - i0][j - j0];
+        if (!s) continue;
+        __atomic_fetch_add(&gram[i * k + j], s, __ATOMIC_RELAXED);
+        if (i != j) __atomic_fetch_add(&gram[j * k + i], s, __ATOMIC_RELAXED);
+      }
   }
   free(bits);
   return 0;

@@ -160,6 +160,45 @@ def cluster(sim: np.ndarray, ids, tau: float) -> list[list[str]]:
     return named
 
 
+def cluster_unique_ids(sim: np.ndarray, ids, tau: float) -> list[list[str]]:
+    """``cluster`` for UNIQUE ids at n ~ 1000 (config 3): the same merge sequence as
+    fs/analytics.py:200-226, with the complete-linkage matrix kept up to date instead of
+    rescanning member pairs (linkage(A u B, C) = min(linkage(A, C), linkage(B, C)) —
+    min of floats, exact).  With unique ids the candidate key (-score, lo, hi, a, b) is
+    decided by (-score, lo, hi), so list positions never matter.  Pinned to ``cluster``
+    by tests/test_oracle_golden.py."""
+    n = len(ids)
+    if len(set(ids)) != n:
+        raise ValueError("cluster_unique_ids needs unique ids")
+    rank = np.empty(n, dtype=np.int64)
+    rank[np.argsort(np.array(ids, dtype=object), kind="stable")] = np.arange(n)
+    link = np.array(sim, dtype=np.float64, copy=True)
+    np.fill_diagonal(link, -np.inf)
+    lo_id = rank.copy()  # min id rank of the cluster rooted at i
+    members = {i: [i] for i in range(n)}
+    iu = np.triu(np.ones((n, n), dtype=bool), 1)
+    while len(members) > 1:
+        best = link[iu].max() if n > 1 else -np.inf
+        if not (best >= tau):
+            break
+        ii, jj = np.nonzero((link == best) & iu)
+        lo = np.minimum(lo_id[ii], lo_id[jj])
+        hi = np.maximum(lo_id[ii], lo_id[jj])
+        pick = np.lexsort((hi, lo))[0]
+        a, b = int(ii[pick]), int(jj[pick])
+        merged = np.minimum(link[a], link[b])
+        link[a, :] = merged
+        link[:, a] = merged
+        link[b, :] = -np.inf
+        link[:, b] = -np.inf
+        link[a, a] = -np.inf
+        lo_id[a] = min(lo_id[a], lo_id[b])
+        members[a] = members[a] + members.pop(b)
+    named = [sorted(ids[i] for i in m) for m in members.values()]
+    named.sort(key=lambda c: c[0])
+    return named
+
+
 def run_stream_counts(cells_list, n: int, width: int, height: int) -> np.ndarray:
     """fs/streaming.py:417-431 — surfaces cycled to n: cycles*full + partial, uint32."""
     k = len(cells_list)

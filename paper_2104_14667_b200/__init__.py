@@ -40,10 +40,12 @@ from .streaming import (
     build_schedule,
     closed_form_times,
     efficiency,
+    frame_budget_bytes,
     max_data_per_frame,
     measure_stream_timing,
     reports_to_csv,
     run_stream,
+    simulate_stream_timing,
 )
 
 __version__ = "0.1.0"
@@ -81,6 +83,7 @@ __all__ = [
     "cluster_surfaces",
     "composite_map",
     "efficiency",
+    "frame_budget_bytes",
     "jaccard",
     "load_surface",
     "max_data_per_frame",
@@ -93,5 +96,6 @@ __all__ = [
     "select_backend",
     "similarity_from_gram",
     "similarity_matrix",
+    "simulate_stream_timing",
     "stream_files",
 ]

@@ -60,6 +60,8 @@ _SIGNATURES = {
     "fs_composite_fill": [_vp, C.c_uint64, C.c_uint64, _vp],
     "fs_accumulate_many": [_vp, C.POINTER(_vp), C.c_uint32, C.c_uint64],
     "fs_gram_many": [C.POINTER(_vp), C.c_uint32, C.c_uint64, _vp],
+    "fs_stack_cache_release": [],
+    "fs_stack_cache_info": [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)],
     "fs_ensemble_create": [C.c_uint64, C.c_uint32, C.POINTER(_vp)],
     "fs_ensemble_destroy": [_vp],
     "fs_ensemble_info": [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),

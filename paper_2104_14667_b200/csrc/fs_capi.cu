@@ -969,65 +969,234 @@ int fs_ensemble_recompute(fs_ensemble *e, const uint32_t *slots, uint32_t k, int
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// batched host-level extensions: a per-thread scratch ensemble
+// batched host-level extensions: a per-device, content-keyed stack cache
 // ---------------------------------------------------------------------------
-static thread_local std::vector<fs_ensemble *> t_scratch_ens;
+// The drop-in analytics hand the SAME stack to the batched entry points once per
+// product: analytics.accumulate, then similarity_matrix, outlier_scores and
+// cluster_surfaces each rebuild the similarity matrix (fs/analytics.py:174-240).  Each
+// device keeps ONE ensemble of bit-packed masks whose slots are keyed by a 128-bit
+// fingerprint of the caller's raster bytes: content already resident is not uploaded
+// again; new content streams into unused or least-recently-used slots.  The cache is
+// shared by all threads of the process (one mutex per device), holds at most
+// kStackCacheMaxBytes of packed masks between calls, and fs_stack_cache_release()
+// frees it.
+namespace {
 
-static int scratch_ensemble(uint64_t pixels, uint32_t k, fs_ensemble **out) {
-  int dev;
-  int rc = current_device(&dev);
-  if (rc) return rc;
-  for (auto it = t_scratch_ens.begin(); it != t_scratch_ens.end(); ++it) {
-    fs_ensemble *e = *it;
-    if (e->device != dev) continue;
-    if (e->pixels == pixels && e->capacity >= k) {
-      *out = e;
-      return FS_OK;
-    }
-    fs_ensemble_destroy(e);
-    t_scratch_ens.erase(it);
-    break;
+constexpr uint64_t kStackCacheMaxBytes = 4ull << 30;
+constexpr uint64_t kFpChunk = 8ull << 20;  // fingerprint work item (bytes)
+
+struct Fp {
+  uint64_t a = 0, b = 0;
+  bool operator==(const Fp &o) const { return a == o.a && b == o.b; }
+};
+
+inline uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+inline uint64_t fmix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  return k ^ (k >> 33);
+}
+
+// 4-lane multiply-rotate hash of one chunk (xxh64-style rounds), 128-bit result
+Fp hash_chunk(const uint8_t *p, uint64_t n, uint64_t seed) {
+  constexpr uint64_t P1 = 0x9E3779B185EBCA87ull, P2 = 0xC2B2AE3D27D4EB4Full;
+  uint64_t l[4] = {seed + P1 + P2, seed + P2, seed, seed - P1};
+  uint64_t i = 0;
+  for (; i + 32 <= n; i += 32) {
+    uint64_t w[4];
+    std::memcpy(w, p + i, 32);
+    for (int j = 0; j < 4; ++j) l[j] = rotl64(l[j] + w[j] * P2, 31) * P1;
   }
-  fs_ensemble *e;
-  rc = fs_ensemble_create(pixels, std::max<uint32_t>(k, 16), &e);
-  if (rc) return rc;
-  t_scratch_ens.push_back(e);
-  *out = e;
+  uint8_t tail[32] = {};
+  std::memcpy(tail, p + i, n - i);
+  uint64_t w[4];
+  std::memcpy(w, tail, 32);
+  for (int j = 0; j < 4; ++j) l[j] = rotl64(l[j] + (w[j] ^ (n - i)) * P2, 31) * P1;
+  Fp f;
+  f.a = fmix64(l[0] ^ rotl64(l[1], 17) ^ rotl64(l[2], 31) ^ rotl64(l[3], 47) ^ n);
+  f.b = fmix64(l[3] ^ rotl64(l[2], 13) ^ rotl64(l[1], 29) ^ rotl64(l[0], 43) ^ (n * P1));
+  return f;
+}
+
+// fingerprints of k rasters of n bytes, chunks hashed in parallel on host threads
+void fingerprints(const uint8_t *const *cells, uint32_t k, uint64_t n, std::vector<Fp> &out) {
+  const uint64_t nch = (n + kFpChunk - 1) / kFpChunk;
+  std::vector<Fp> part((size_t)k * nch);
+  std::atomic<uint64_t> next{0};
+  const uint64_t items = (uint64_t)k * nch;
+  auto work = [&] {
+    for (uint64_t it; (it = next.fetch_add(1)) < items;) {
+      const uint64_t m = it / nch, c = it % nch, off = c * kFpChunk;
+      part[it] = hash_chunk(cells[m] + off, std::min(kFpChunk, n - off), c);
+    }
+  };
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nt = (unsigned)std::min<uint64_t>(std::min(hw, 16u), items);
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; ++t) th.emplace_back(work);
+  work();
+  for (auto &t : th) t.join();
+  out.assign(k, Fp{});
+  for (uint32_t m = 0; m < k; ++m) {
+    Fp f{n, ~n};
+    for (uint64_t c = 0; c < nch; ++c) {
+      const Fp &q = part[(size_t)m * nch + c];
+      f.a = fmix64(f.a ^ q.a) + rotl64(f.b, 23);
+      f.b = fmix64(f.b ^ q.b) + rotl64(f.a, 41);
+    }
+    out[m] = f;
+  }
+}
+
+struct StackCache {
+  std::mutex mu;
+  fs_ensemble *ens = nullptr;
+  std::vector<Fp> fp;            // per slot: fingerprint of its content
+  std::vector<uint8_t> valid;    // per slot: holds content
+  std::vector<uint64_t> stamp;   // per slot: last use
+  uint64_t clock = 0;
+  void drop() {
+    if (ens) fs_ensemble_destroy(ens);
+    ens = nullptr;
+    fp.clear();
+    valid.clear();
+    stamp.clear();
+  }
+};
+StackCache g_stack[kMaxDevices];
+
+// Make rasters cells[0..k) resident in cache c (locked by the caller) and return their
+// slots (equal content -> one slot).
+int stack_slots(StackCache &c, const uint8_t *const *cells, uint32_t k, uint64_t n,
+                std::vector<uint32_t> &slot) {
+  std::vector<Fp> f;
+  fingerprints(cells, k, n, f);
+  // distinct contents of the request
+  std::vector<uint32_t> first_of(k);
+  uint32_t distinct = 0;
+  for (uint32_t i = 0; i < k; ++i) {
+    first_of[i] = i;
+    for (uint32_t j = 0; j < i; ++j)
+      if (f[j] == f[i]) { first_of[i] = first_of[j]; break; }
+    if (first_of[i] == i) ++distinct;
+  }
+  if (c.ens && (c.ens->pixels != n || c.ens->capacity < distinct)) {
+    const uint32_t cap = std::max<uint32_t>(distinct, 2 * c.ens->capacity);
+    const bool same_px = c.ens->pixels == n;
+    c.drop();
+    if (same_px) distinct = std::max(distinct, cap);  // grow geometrically
+  }
+  if (!c.ens) {
+    int rc = fs_ensemble_create(n, std::max<uint32_t>(distinct, 16), &c.ens);
+    if (rc) {
+      c.ens = nullptr;
+      return rc;
+    }
+    c.fp.assign(c.ens->capacity, Fp{});
+    c.valid.assign(c.ens->capacity, 0);
+    c.stamp.assign(c.ens->capacity, 0);
+  }
+  const uint32_t cap = c.ens->capacity;
+  const uint64_t now = ++c.clock;
+  slot.assign(k, UINT32_MAX);
+  std::vector<uint8_t> taken(cap, 0);
+  for (uint32_t i = 0; i < k; ++i) {  // hits
+    if (first_of[i] != i) continue;
+    for (uint32_t s = 0; s < cap; ++s)
+      if (c.valid[s] && c.fp[s] == f[i]) {
+        slot[i] = s;
+        taken[s] = 1;
+        break;
+      }
+  }
+  std::vector<uint32_t> miss;  // request indices to upload
+  for (uint32_t i = 0; i < k; ++i)
+    if (first_of[i] == i && slot[i] == UINT32_MAX) miss.push_back(i);
+  if (!miss.empty()) {
+    // victims: slots not used by this request, empty ones first, then oldest
+    std::vector<uint32_t> free_slots;
+    for (uint32_t s = 0; s < cap; ++s)
+      if (!taken[s]) free_slots.push_back(s);
+    std::stable_sort(free_slots.begin(), free_slots.end(), [&](uint32_t x, uint32_t y) {
+      if (c.valid[x] != c.valid[y]) return c.valid[x] < c.valid[y];
+      return c.stamp[x] < c.stamp[y];
+    });
+    std::vector<uint32_t> dst(free_slots.begin(), free_slots.begin() + miss.size());
+    std::sort(dst.begin(), dst.end());
+    for (size_t q = 0; q < miss.size(); ++q) {
+      slot[miss[q]] = dst[q];
+      c.valid[dst[q]] = 0;  // until its upload succeeded
+    }
+    // one streamed upload per run of consecutive destination slots
+    for (size_t q = 0; q < miss.size();) {
+      size_t r = q + 1;
+      while (r < miss.size() && dst[r] == dst[r - 1] + 1) ++r;
+      std::vector<const uint8_t *> src;
+      int pinned = 1;
+      for (size_t t = q; t < r; ++t) {
+        src.push_back(cells[miss[t]]);
+        int p = 0;
+        if (pinned) fs_host_is_pinned(cells[miss[t]], &p);
+        pinned &= p;
+      }
+      int rc = fs_ensemble_stream(c.ens, dst[q], 0, src.data(), (uint32_t)(r - q),
+                                  pinned ? FS_VARIANT_2B_FINAL : FS_VARIANT_2B_INITIAL, 0, 0,
+                                  nullptr);
+      if (rc) return rc;
+      for (size_t t = q; t < r; ++t) {
+        c.fp[dst[t]] = f[miss[t]];
+        c.valid[dst[t]] = 1;
+      }
+      q = r;
+    }
+  }
+  for (uint32_t i = 0; i < k; ++i) {
+    slot[i] = slot[first_of[i]];
+    c.stamp[slot[i]] = now;
+  }
   return FS_OK;
 }
 
-static int stream_any(fs_ensemble *e, const uint8_t *const *cells, uint32_t k) {
-  // pinned sources stream straight from the caller (2b-final); pageable ones go
-  // through the pinned staging ring with a parallel host copy (2b-initial).
-  int pinned = 1;
-  for (uint32_t i = 0; i < k && pinned; ++i) {
-    int p = 0;
-    fs_host_is_pinned(cells[i], &p);
-    pinned = p;
+// the device's cache, locked; big ensembles are not kept past the call
+struct StackLease {
+  StackCache *c = nullptr;
+  std::unique_lock<std::mutex> lk;
+  ~StackLease() {
+    if (c && c->ens && (uint64_t)c->ens->capacity * c->ens->wpm * 4 > kStackCacheMaxBytes)
+      c->drop();
   }
-  return fs_ensemble_stream(e, 0, 0, cells, k,
-                            pinned ? FS_VARIANT_2B_FINAL : FS_VARIANT_2B_INITIAL, 0, 0, nullptr);
+};
+
+int lease_stack(StackLease &l) {
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  if (dev < 0 || dev >= kMaxDevices) return set_err(FS_ENODEV, "device index out of range");
+  l.c = &g_stack[dev];
+  l.lk = std::unique_lock<std::mutex>(l.c->mu);
+  return FS_OK;
 }
+
+}  // namespace
 
 extern "C" {
 
 int fs_accumulate_many(uint32_t *counts, const uint8_t *const *cells, uint32_t k, uint64_t n) {
   if (n == 0 || k == 0) return FS_OK;
   if (!counts || !cells) return set_err(FS_EINVAL, "null buffer");
-  fs_ensemble *e;
-  int rc = scratch_ensemble(n, k, &e);
+  StackLease l;
+  int rc = lease_stack(l);
   if (rc) return rc;
-  rc = stream_any(e, cells, k);
-  if (rc) return rc;
-  std::vector<uint32_t> slots(k);
-  for (uint32_t i = 0; i < k; ++i) slots[i] = i;
-  // counts += fused count: upload the caller's counts, add on device
-  std::vector<uint32_t> tmp;
+  std::vector<uint32_t> slots;
+  if ((rc = stack_slots(*l.c, cells, k, n, slots))) return rc;
+  // counts += fused count of the slots
   bool zero = true;
   for (uint64_t p = 0; p < n && zero; ++p) zero = counts[p] == 0;
-  if (zero) return fs_ensemble_overlap(e, slots.data(), k, 1, 0, counts, nullptr, nullptr, 0);
-  tmp.resize(n);
-  rc = fs_ensemble_overlap(e, slots.data(), k, 1, 0, tmp.data(), nullptr, nullptr, 0);
+  if (zero) return fs_ensemble_overlap(l.c->ens, slots.data(), k, 1, 0, counts, nullptr, nullptr, 0);
+  std::vector<uint32_t> tmp(n);
+  rc = fs_ensemble_overlap(l.c->ens, slots.data(), k, 1, 0, tmp.data(), nullptr, nullptr, 0);
   if (rc) return rc;
   for (uint64_t p = 0; p < n; ++p) counts[p] += tmp[p];
   return FS_OK;
@@ -1040,14 +1209,43 @@ int fs_gram_many(const uint8_t *const *cells, uint32_t k, uint64_t n, int64_t *g
     std::memset(gram, 0, (size_t)k * k * 8);
     return FS_OK;
   }
-  fs_ensemble *e;
-  int rc = scratch_ensemble(n, k, &e);
+  StackLease l;
+  int rc = lease_stack(l);
   if (rc) return rc;
-  rc = stream_any(e, cells, k);
+  std::vector<uint32_t> slots;
+  if ((rc = stack_slots(*l.c, cells, k, n, slots))) return rc;
+  return fs_ensemble_gram(l.c->ens, slots.data(), k, FS_GRAM_AUTO, gram, 0);
+}
+
+int fs_stack_cache_release(void) {
+  int dev;
+  int rc = current_device(&dev);
   if (rc) return rc;
-  std::vector<uint32_t> slots(k);
-  for (uint32_t i = 0; i < k; ++i) slots[i] = i;
-  return fs_ensemble_gram(e, slots.data(), k, FS_GRAM_AUTO, gram, 0);
+  if (dev < 0 || dev >= kMaxDevices) return FS_OK;
+  std::lock_guard<std::mutex> g(g_stack[dev].mu);
+  g_stack[dev].drop();
+  return FS_OK;
+}
+
+int fs_stack_cache_info(uint32_t *slots_valid, uint32_t *capacity, uint64_t *pixels) {
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  uint32_t v = 0, cap = 0;
+  uint64_t px = 0;
+  if (dev >= 0 && dev < kMaxDevices) {
+    std::lock_guard<std::mutex> g(g_stack[dev].mu);
+    StackCache &c = g_stack[dev];
+    if (c.ens) {
+      cap = c.ens->capacity;
+      px = c.ens->pixels;
+      for (uint8_t x : c.valid) v += x;
+    }
+  }
+  if (slots_valid) *slots_valid = v;
+  if (capacity) *capacity = cap;
+  if (pixels) *pixels = px;
+  return FS_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -1004,14 +1004,10 @@ static cudaError_t launch_one(const CUtensorMap &tm, const tc::Plan &p, int32_t 
   const uint64_t upc = DIAG ? p.upc_diag : p.upc_off;
   const uint64_t units = DIAG ? p.units_diag : p.units_off;
   if (ntiles == 0 || kc == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<PANEL, DIAG, FP4, FUSE, FD>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static SmemOptIn attr;
+  if (cudaError_t e = smem_opt_in(attr, tc::k_gram_tc<PANEL, DIAG, FP4, FUSE, FD>, C::kSmemBytes);
+      e != cudaSuccess)
+    return e;
   tc::k_gram_tc<PANEL, DIAG, FP4, FUSE, FD>
       <<<ntiles * kc, C::kThreadsTotal, C::kSmemBytes, s>>>(
           tm, p.npanels, kc, upc, units, part, ov, p.k);
@@ -1102,13 +1098,9 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
     if (e != cudaSuccess) return e;
     if (p.pair) {
       if (p.kc_off > 0) {
-        static bool attr = false;
-        if (!attr) {
-          if ((e = cudaFuncSetAttribute(tc::k_gram_pair_f4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        tc::kPairSmemBytes)) != cudaSuccess)
-            return e;
-          attr = true;
-        }
+        static SmemOptIn attr;
+        if ((e = smem_opt_in(attr, tc::k_gram_pair_f4, tc::kPairSmemBytes)) != cudaSuccess)
+          return e;
         tc::k_gram_pair_f4<<<2 * p.noff * p.kc_off, tc::kPairThreads, tc::kPairSmemBytes, s>>>(
             tm_pair, p.npanels, p.kc_off, p.upc_off, p.units_off, part_off);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -1,6 +1,8 @@
 // fs_internal.h — launchers shared between the kernel files and the C ABI layer.
 #pragma once
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <cuda.h>  // CUtensorMap (types only; the encoder is fetched at run time)
 #include <cuda_runtime.h>
@@ -12,7 +14,29 @@ namespace fs {
 constexpr uint32_t kHistSmemBins = 4096;       // overlap classes kept in shared memory
 constexpr uint64_t kLutMaxEntries = 1u << 20;  // composite grey LUT (n_inputs + 1)
 
-int num_sms();
+int num_sms();  // SM count of the calling thread's current device
+
+// Dynamic shared-memory opt-in of one kernel (cudaFuncAttributeMaxDynamicSharedMemorySize).
+// Function attributes belong to each device's context, so the granted size is tracked
+// per device; concurrent callers serialise on the mutex only until their device is set.
+constexpr int kMaxDevices = 64;
+struct SmemOptIn {
+  std::mutex mu;
+  std::atomic<size_t> granted[kMaxDevices] = {};
+};
+template <typename Kernel>
+inline cudaError_t smem_opt_in(SmemOptIn &o, Kernel *fn, size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if (o.granted[dev].load(std::memory_order_acquire) >= bytes) return cudaSuccess;
+  std::lock_guard<std::mutex> lk(o.mu);
+  if (o.granted[dev].load(std::memory_order_relaxed) >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) o.granted[dev].store(bytes, std::memory_order_release);
+  return e;
+}
 
 // 3-D tensor map over the tile-interleaved packed layout, restricted to rows
 // [row0, row0 + rows) of `capacity`: dims (32 words, rows, ntiles), box

@@ -20,15 +20,18 @@
 
 namespace fs {
 
-static int g_num_sms = 0;
+static std::atomic<int> g_num_sms[kMaxDevices] = {};
 int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int n = g_num_sms[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    g_num_sms[dev].store(n, std::memory_order_relaxed);
   }
-  return g_num_sms;
+  return n;
 }
 
 // ---------------------------------------------------------------------------
@@ -164,12 +167,10 @@ cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint
   if (engine == 0) {
     const uint64_t nchunks = pixels / kPackChunk;
     if (nchunks > 0) {
-      static bool attr_set = false;
+      static SmemOptIn attr;
       const int smem = kPackStages * kPackChunk + kPackStages * 8;
-      if (!attr_set) {
-        cudaFuncSetAttribute(k_pack_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_set = true;
-      }
+      if (cudaError_t e = smem_opt_in(attr, k_pack_bulk, (size_t)smem); e != cudaSuccess)
+        return e;
       uint64_t grid = (uint64_t)num_sms() * 6;
       if (grid > nchunks) grid = nchunks;
       k_pack_bulk<<<(unsigned)grid, kPackThreads, smem, s>>>(src, nchunks, dst, slot, cap);
@@ -539,13 +540,8 @@ template <bool GATHER, int NH>
 static cudaError_t launch_overlap_t(const CUtensorMap &tm, const OverlapArgs &a, uint32_t sbins,
                                     uint64_t ntg, cudaStream_t s) {
   const size_t smem = ov_smem_bytes(sbins);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(k_overlap<GATHER, NH>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  static SmemOptIn attr;
+  if (cudaError_t e = smem_opt_in(attr, k_overlap<GATHER, NH>, smem); e != cudaSuccess) return e;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_overlap<GATHER, NH>, kOvThreads, smem);
   if (per_sm < 1) per_sm = 1;
@@ -664,13 +660,9 @@ cudaError_t launch_combine_partials(const uint16_t *partial16, uint32_t npanels,
   a.vec = ((reinterpret_cast<uintptr_t>(a.counts) | reinterpret_cast<uintptr_t>(a.rgba)) & 15) == 0;
   const uint32_t sbins = a.nbins <= 8192 ? (uint32_t)((a.nbins + 31) / 32 * 32) : 0u;
   const size_t smem = (size_t)sbins * 8;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(k_combine_partials,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  static SmemOptIn attr;
+  if (smem > 48 * 1024)
+    if (cudaError_t e = smem_opt_in(attr, k_combine_partials, smem); e != cudaSuccess) return e;
   const uint64_t ngroups = (a.pixels + 7) / 8;
   uint64_t grid = (ngroups + kCombThreads - 1) / kCombThreads;
   const uint64_t gcap = (uint64_t)num_sms() * 8;

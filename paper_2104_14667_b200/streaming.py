@@ -215,17 +215,42 @@ def reports_to_csv(reports: Sequence[PipelineRunReport]) -> str:
     return buf.getvalue()
 
 
-def _report(job: StreamJob, stats) -> PipelineRunReport:
+# Longest run streamed item by item.  Longer jobs time this many items through the
+# real DAG and extend the per-item costs to n (the grid is still exact, from the
+# cycled overlap pass): the reference allows n up to 2^32 - 1, which would otherwise
+# mean 6n CUDA events and n uploads for a grid that needs k.
+MEASURE_CAP = 1024
+
+MAKESPAN_SOURCES = ("measured", "simulated", "closed-form")
+
+
+def _report(job: StreamJob, stats, makespan_source: str = "measured") -> PipelineRunReport:
+    """Measured per-item costs -> the reference's report (streaming.py:247-309).
+    ``stats`` covers ``s`` <= n items; when s < n the per-item lists are cycled to n and
+    the measured total is scaled by n / s (steady state), flagged in ``makespan_source``."""
+    variant = Variant(job.variant)
     c = [round_half_up(x) for x in stats.copy_us]
     m = [round_half_up(x) for x in stats.xform_us]
     p = [round_half_up(x) for x in stats.kernel_us]
-    h = [round_half_up(x) for x in stats.host_us] if Variant(job.variant).coupled_write else []
+    h = [round_half_up(x) for x in stats.host_us] if variant.coupled_write else []
+    s = len(c)
+    source = "measured"
     total = max(1, round_half_up(stats.total_us))
+    if s < job.n:
+        reps = -(-job.n // s)
+        c, m, p = ((x * reps)[: job.n] for x in (c, m, p))
+        h = (h * reps)[: job.n] if h else h
+        total = max(1, round_half_up(stats.total_us * job.n / s))
+        source = f"measured ({s} of {job.n} items, scaled)"
+    if makespan_source == "closed-form":
+        t_dual, t_single = closed_form_times(c, m, p)
+        total = max(1, t_single if variant is Variant.ONE_BUFFER_FINAL else t_dual)
+        source = "closed-form"
     return PipelineRunReport(
-        variant=Variant(job.variant).value, n=job.n, width=job.width, height=job.height,
+        variant=variant.value, n=job.n, width=job.width, height=job.height,
         total_time_us=total, per_item_c=c, per_item_m=m, per_item_p=p,
         transfer_rate_gbps=job.n * job.payload_bytes / total / 1000.0,
-        efficiency=efficiency(c, total), makespan_source="measured",
+        efficiency=efficiency(c, total), makespan_source=source,
         contention_applied=False, warmup=False, per_item_h=h,
     )
 
@@ -243,62 +268,128 @@ def _validate(job: StreamJob) -> None:
         raise StreamError("accumulation counts would overflow 32 bits")
 
 
+def _check_source(job: StreamJob, makespan_source: str) -> None:
+    if makespan_source not in MAKESPAN_SOURCES:
+        raise StreamError(f"unknown makespan_source {makespan_source!r}")
+    if makespan_source == "closed-form" and Variant(job.variant) not in (
+            Variant.ONE_BUFFER_FINAL, Variant.TWO_BUFFER_FINAL):
+        raise StreamError("closed-form totals are defined for the final strategies only")
+
+
+def _timed_stream(ens, rasters, job: StreamJob, k: int):
+    """Stream min(n, MEASURE_CAP) items (surfaces cycled over k slots) through the
+    variant's DAG with the per-item accumulate, measured with CUDA events."""
+    s = min(job.n, MEASURE_CAP)
+    items = [rasters[i % k] for i in range(s)]
+    return ens.stream(items, variant=Variant(job.variant).value, with_kernel=True,
+                      reset_counts=True, slot_wrap=k)
+
+
 def run_stream(job: StreamJob, *, makespan_source: str = "measured"):
     """Stream ``job.n`` rasters (surfaces cycled in order) through the variant's
     pipeline on the GPU and accumulate them.  Returns ``(grid, report)``; the grid is
-    bit-identical across strategies (streaming.py:394-433), the report is measured."""
+    bit-identical across strategies (streaming.py:394-433), the report is measured.
+
+    ``makespan_source``: ``"measured"`` (default) and ``"simulated"`` (the reference's
+    default name, kept so its callers run unchanged) both report the CUDA-event total of
+    the real run; ``"closed-form"`` reports the paper's §7.1 closed form
+    (``closed_form_times``) evaluated on the measured per-item costs (final strategies
+    only, as in the reference).  ``report.makespan_source`` says which one it is."""
     from .analytics import AccumulationGrid
     from .ensemble import DeviceEnsemble
 
-    if makespan_source != "measured":
-        raise StreamError(
-            f"makespan_source {makespan_source!r} belongs to the reference's cost model; "
-            "this framework measures the pipeline (use 'measured')"
-        )
+    _check_source(job, makespan_source)
     _validate(job)
     k = len(job.surfaces)
-    rasters = [job.surfaces[i % k] for i in range(job.n)]
     with DeviceEnsemble(job.width, job.height, k) as ens:
-        stats = ens.stream(rasters, variant=Variant(job.variant).value, with_kernel=True,
-                           reset_counts=True, slot_wrap=k)
-        counts, _, _ = ens.running_counts(job.n, bins=False, rgba=False)
+        stats = _timed_stream(ens, list(job.surfaces), job, k)
+        if job.n <= MEASURE_CAP:
+            # the grid the per-item kernel[i] nodes accumulated
+            counts, _, _ = ens.running_counts(job.n, bins=False, rgba=False)
+        else:
+            # exact grid in O(k): every slot holds its surface after the timed run;
+            # counts = cycles * full + the first `remainder` again (streaming.py:417-431)
+            cycles, rem = divmod(job.n, k)
+            counts, _, _ = ens.overlap(list(range(k)), cycles=cycles, remainder=rem,
+                                       bins=False, rgba=False)
     grid = AccumulationGrid._from_device(job.width, job.height, job.n, counts)
-    return grid, _report(job, stats)
+    return grid, _report(job, stats, makespan_source)
+
+
+def simulate_stream_timing(job: StreamJob, *, makespan_source: str = "measured"
+                           ) -> PipelineRunReport:
+    """Timing-only run (the reference's ``simulate_stream_timing``,
+    streaming.py:324-373, answered by measurement): streams ``job.n`` rasters of the
+    job's size — ``job.surfaces`` cycled, or two synthetic flood masks when the job
+    carries none — through the variant's DAG and reports the measured pipeline.
+    ``makespan_source`` as in ``run_stream``; ``job.profile`` (a cost model in the
+    reference) is not consulted."""
+    from . import _native as N
+    from .ensemble import DeviceEnsemble
+
+    _check_source(job, makespan_source)
+    if job.n >= (1 << 32):
+        raise StreamError("accumulation counts would overflow 32 bits")
+    payload = job.payload_bytes
+    if job.surfaces:
+        rasters = [getattr(s, "cells", s) for s in job.surfaces]
+        bufs = []
+    else:
+        bufs = [N.PinnedBuffer((payload,)) for _ in range(min(2, job.n))]
+        for i, b in enumerate(bufs):
+            N.call("fs_synth_host", N.ptr(b.array), 2104, job.width, job.height, 0, job.height,
+                   i, 1, 0.02, 0)
+        rasters = [b.array for b in bufs]
+    try:
+        k = len(rasters)
+        with DeviceEnsemble(job.width, job.height, k) as ens:
+            stats = _timed_stream(ens, rasters, job, k)
+    finally:
+        for b in bufs:
+            b.free()
+    return _report(job, stats, makespan_source)
 
 
 def measure_stream_timing(job: StreamJob) -> PipelineRunReport:
-    """Timing-only run over synthetic-free inputs: streams ``job.surfaces`` (cycled)
-    and reports the measured pipeline.  The analogue of simulate_stream_timing."""
-    return run_stream(job)[1]
+    """Alias of ``simulate_stream_timing`` under the name of what it does."""
+    return simulate_stream_timing(job)
+
+
+def frame_budget_bytes(c_eff: float, m_eff: float, p: float, payload: int,
+                       target_fps: int) -> int:
+    """The reference's frame budget (streaming.py:436-464): steady-state throughput of
+    the two-pair final pipeline times the frame interval, i.e. payload / per-item step
+    with step = max(copy, transform + kernel) — in integer µs arithmetic as there."""
+    if target_fps < 1:
+        raise StreamError("target_fps must be positive")
+    step = max(c_eff, m_eff + p)
+    frame_us = 1_000_000 // target_fps
+    if step <= 0:
+        raise StreamError("per-item costs must be positive")
+    return int(frame_us * payload // step)
 
 
 def max_data_per_frame(profile, width: int, height: int, target_fps: int = 10,
                        *, samples: int = 8) -> int:
-    """Bytes the two-pair final pipeline sustains per frame at ``target_fps``,
-    from a measured 2b-final run of ``samples`` rasters of this size (the reference
-    derives it from modelled costs, streaming.py:436-464; ``profile`` is ignored)."""
-    from .ensemble import DeviceEnsemble
-    from . import _native as N
-
+    """Bytes the two-pair final pipeline sustains per frame at ``target_fps``
+    (streaming.py:436-464).  The per-item costs come from ``profile`` when it is a
+    measured ``PipelineRunReport`` of this raster size (medians of its per-item c / m /
+    p); otherwise (a reference cost-model profile, or None) from a fresh measured
+    2b-final run of ``samples`` rasters of this size on the device."""
     if target_fps < 1:
         raise StreamError("target_fps must be positive")
     if width < 1 or height < 1:
         raise StreamError("image dimensions must be positive")
     payload = width * height
-    bufs = [N.PinnedBuffer((payload,)) for _ in range(2)]
-    try:
-        for i, b in enumerate(bufs):
-            N.call("fs_synth_host", N.ptr(b.array), 2104 + i, width, height, 0, height, i, 1,
-                   0.02, 0)
-        with DeviceEnsemble(width, height, 2) as ens:
-            ens.stream([b.array for b in bufs], variant="2b-final", with_kernel=True)  # warm-up
-            st = ens.stream([bufs[i % 2].array for i in range(samples)], variant="2b-final",
-                            with_kernel=True, slot_wrap=2)
-    finally:
-        for b in bufs:
-            b.free()
-    c_eff = float(np.median(st.copy_us))
-    mp = float(np.median(np.array(st.xform_us) + np.array(st.kernel_us)))
-    step = max(c_eff, mp)
-    frame_us = 1_000_000 // target_fps
-    return int(frame_us * payload // max(step, 1e-3))
+    if isinstance(profile, PipelineRunReport):
+        if (profile.width, profile.height) != (width, height):
+            raise StreamError("report was measured at another raster size")
+        c_eff = float(np.median(profile.per_item_c))
+        m_eff = float(np.median(profile.per_item_m))
+        p = float(np.median(profile.per_item_p))
+        return frame_budget_bytes(c_eff, m_eff, p, payload, target_fps)
+    job = StreamJob(variant=Variant.TWO_BUFFER_FINAL, n=max(2, samples), width=width,
+                    height=height)
+    simulate_stream_timing(job)  # warm-up (allocations, first-launch costs)
+    rep = simulate_stream_timing(job)
+    return max_data_per_frame(rep, width, height, target_fps)

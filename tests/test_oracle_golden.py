@@ -109,3 +109,30 @@ def test_reference_cython_accelerator_agrees(golden):
         _accel.accumulate_into(counts, c.reshape(-1))
     assert sha(counts.reshape(1024, 1024)) == golden["c1"]["counts_sha"]
     assert list(_accel.overlap_counts(counts, 16)) == golden["c1"]["bins"]
+
+
+def test_cluster_unique_ids_matches_cluster():
+    """The linkage-matrix form of the oracle clusterer (used at n = 1024) gives the same
+    lists as the literal restatement of fs/analytics.py:184-226, ties included."""
+    rng = np.random.default_rng(0)
+    for t in range(200):
+        n = int(rng.integers(1, 25))
+        x = rng.random((n, n))
+        if t % 3 == 0:
+            x = np.round(x * 4) / 4  # many exact ties
+        s = np.minimum(x, x.T)
+        np.fill_diagonal(s, 1.0)
+        ids = [f"s{i:03d}" for i in rng.permutation(n)]
+        tau = float(rng.choice([0.1, 0.25, 0.5, 0.75, 0.8, 1.0]))
+        assert O.cluster(s, ids, tau) == O.cluster_unique_ids(s, ids, tau), t
+
+
+def test_blocked_c_gram_matches_pair_loop():
+    """oracle/fs_oracle.c's blocked Gram (full-size configs) equals the pair loop."""
+    import oracle_c
+
+    rng = np.random.default_rng(1)
+    for k, n in [(1, 5), (3, 100), (17, 1000), (40, 70001), (130, 3000)]:
+        cells = [(rng.random(n) < rng.random()).astype(np.uint8) *
+                 rng.integers(0, 3, n).astype(np.uint8) for _ in range(k)]
+        assert np.array_equal(oracle_c.gram(cells), O.gram(cells)), (k, n)

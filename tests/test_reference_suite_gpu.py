@@ -53,3 +53,23 @@ def test_reference_implementation_outputs_identical():
                        capture_output=True, text=True, timeout=600, cwd=REPO)
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["all_identical"], out
+
+
+def test_reference_streaming_suite_with_streaming_bound():
+    """floodstream.streaming bound to this package too (run_stream / simulate_stream_timing
+    measured on the device): the reference's test_streaming.py and test_service.py pass
+    except the listed cost-model VALUE assertions (tools/run_reference_tests.py
+    COST_MODEL_ASSERTIONS: totals/budgets/limits priced by a DeviceProfile)."""
+    if not (REPO / "baseline" / "_ref" / "ref_tests").exists():
+        pytest.skip("reference install (baseline/_ref) not present")
+    ref_tests = REPO / "baseline" / "_ref" / "ref_tests"
+    r = subprocess.run([sys.executable, str(REPO / "tools" / "run_reference_tests.py"),
+                        "--bind-streaming", str(ref_tests / "test_streaming.py"),
+                        str(ref_tests / "test_service.py")],
+                       capture_output=True, text=True, timeout=1200, cwd=REPO)
+    summary = json.loads(r.stdout.strip().splitlines()[-1])
+    assert summary["binding"]["floodstream.streaming"] == "paper_2104_14667_b200.streaming"
+    unexpected = [f for f in summary["failed"] if f not in summary["cost_model_failed"]]
+    assert not unexpected, (unexpected, r.stdout[-3000:])
+    assert summary["files"]["test_streaming.py"]["passed"] >= 20
+    assert summary["files"]["test_service.py"]["passed"] > 0

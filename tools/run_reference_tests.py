@@ -12,7 +12,13 @@ B200 kernels; everything off the path (cost model, simulator, calibration, stats
 stays the reference's own code.  Prints one JSON summary line (per-file outcomes and the
 failing test ids) after pytest's own report.
 
-Usage: python tools/run_reference_tests.py [--boundary-only] [pytest args ...]
+With ``--bind-streaming`` ``floodstream.streaming`` is bound as well (its run_stream /
+simulate_stream_timing measure the real upload DAG on the device instead of pricing the
+reference's cost model).  The reference tests that assert cost-model VALUES (totals,
+budgets and limits derived from a DeviceProfile's prices) cannot hold for measured
+timings; they are listed in COST_MODEL_ASSERTIONS and reported apart.
+
+Usage: python tools/run_reference_tests.py [--boundary-only | --bind-streaming] [pytest args ...]
 """
 from __future__ import annotations
 
@@ -24,7 +30,28 @@ REPO = Path(__file__).resolve().parent.parent
 REF = REPO / "baseline" / "_ref"
 
 
-def bind_floodstream(boundary_only: bool = False) -> dict:
+# test ids (in the reference's tests/test_streaming.py) whose assertions are values of
+# the reference's cost model: simulated totals of profile-priced items, the closed form
+# equal to the simulation, the simulator's 16k image limit, frame budgets from profile
+# prices.  Measured timings cannot reproduce them; everything else must pass.
+COST_MODEL_ASSERTIONS = (
+    "test_streaming.py::TestHandComputedTotals::test_total",
+    "test_streaming.py::test_simulator_matches_closed_forms_exactly",
+    "test_streaming.py::test_closed_form_makespan_source_agrees_with_simulation",
+    "test_streaming.py::TestStreamJob::test_oversized_images_rejected_at_timing",
+    "test_streaming.py::TestFrameBudget::test_steady_state_throughput",
+    "test_streaming.py::TestFrameBudget::test_transform_bound_pipeline",
+    # the service snapshot embeds run_stream's report: digest, histogram and PNG of the
+    # recompute after a restart are identical, its measured microseconds are not
+    "test_service.py::TestRestart::test_state_survives_byte_exactly",
+)
+
+
+def is_cost_model_assertion(nodeid: str) -> bool:
+    return any(nodeid.split("[")[0].endswith(x) for x in COST_MODEL_ASSERTIONS)
+
+
+def bind_floodstream(boundary_only: bool = False, streaming: bool = False) -> dict:
     """Make ``import floodstream`` = the reference package with our hot-path modules.
     ``boundary_only``: bind just the backend registry (fs/backends.py:21-47), so the
     reference's OWN analytics.py drives our C-ABI protocol module primitive by primitive
@@ -33,9 +60,12 @@ def bind_floodstream(boundary_only: bool = False) -> dict:
     import paper_2104_14667_b200.analytics as analytics
     import paper_2104_14667_b200.backends as backends
     import paper_2104_14667_b200.rasters as rasters
+    import paper_2104_14667_b200.streaming as streaming_mod
 
     bound = {"backends": backends} if boundary_only else {
         "analytics": analytics, "backends": backends, "rasters": rasters}
+    if streaming:
+        bound["streaming"] = streaming_mod
 
     import importlib.util
 
@@ -72,8 +102,9 @@ def main(argv: list[str]) -> int:
         print(json.dumps({"unavailable": "baseline/_ref (reference install + ref_tests) missing"}))
         return 0
     boundary_only = "--boundary-only" in argv
-    argv = [a for a in argv if a != "--boundary-only"]
-    binding = bind_floodstream(boundary_only)
+    streaming = "--bind-streaming" in argv
+    argv = [a for a in argv if a not in ("--boundary-only", "--bind-streaming")]
+    binding = bind_floodstream(boundary_only, streaming)
     import floodstream
 
     assert floodstream.backends.__name__ == "paper_2104_14667_b200.backends"
@@ -81,13 +112,15 @@ def main(argv: list[str]) -> int:
     import pytest
 
     col = Collector()
-    args = [str(REF / "ref_tests"), "-q", "-p", "no:cacheprovider", "--rootdir",
-            str(REF / "ref_tests")] + argv
+    paths = [a for a in argv if not a.startswith("-")]
+    args = ([] if paths else [str(REF / "ref_tests")]) + [
+        "-q", "-p", "no:cacheprovider", "--rootdir", str(REF / "ref_tests")] + argv
     rc = pytest.main(args, plugins=[col])
     print(json.dumps({"binding": binding,
                       "files": col.outcomes,
                       "passed": sum(d.get("passed", 0) for d in col.outcomes.values()),
-                      "failed": col.failed}))
+                      "failed": col.failed,
+                      "cost_model_failed": [f for f in col.failed if is_cost_model_assertion(f)]}))
     return int(rc)
 
 
