@@ -108,3 +108,17 @@ def gram_many(cells_list) -> np.ndarray:
             raise ValueError("gram_many needs equally sized arrays")
     N.call("fs_gram_many", N.ptr_array(flats), k, n, N.ptr(gram))
     return gram
+
+
+def stack_cache_info() -> dict:
+    """The calling device's batched-call cache: resident masks, capacity, raster size."""
+    v, cap, px = C.c_uint32(), C.c_uint32(), C.c_uint64()
+    N.call("fs_stack_cache_info", C.byref(v), C.byref(cap), C.byref(px))
+    return {"resident": v.value, "capacity": cap.value, "pixels": px.value}
+
+
+def release_stack_cache() -> None:
+    """Free the calling device's batched-call cache (bit-packed stack kept in HBM so
+    that accumulate -> similarity_matrix -> outlier_scores -> cluster_surfaces upload a
+    stack once; include/floodstream.h fs_stack_cache_release)."""
+    N.call("fs_stack_cache_release")

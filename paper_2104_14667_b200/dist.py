@@ -190,24 +190,24 @@ class ShardedEnsemble:
             part = b["h_part"].numpy()
             k = b["k"]
             out = {"bins": part[: b["nb"]].copy(), "gram": part[b["nb"]:].reshape(k, k).copy()}
+            # copy the frame's analytics out of the pinned slot BEFORE the slot can be
+            # handed back: the main thread reuses it for frame f + depth, whose D2H
+            # would otherwise land under these reads
+            sim = b["h_sim"].numpy().reshape(k, k).copy() if analytics else None
+            scores = b["h_scores"].numpy()[:k].copy() if (analytics and k >= 2) else None
             if maps_to_host:
                 b["event_maps"].synchronize()
                 # views of the pinned slot: valid until the slot is reused (``depth``
                 # frames later) — copy them to keep them longer
                 out["counts"] = b["h_counts"].numpy().view(np.uint32).reshape(self.rows, self.width)
                 out["rgba"] = b["h_rgba"].numpy().reshape(self.rows, self.width, 4)
-            else:
-                if free is not None:
-                    free.set()
-                    free = None
+            elif free is not None:
+                free.set()
+                free = None
             if analytics:
-                sim = b["h_sim"].numpy().reshape(k, k).copy()
                 out["similarity"] = sim
-                if k >= 2:
-                    sc = b["h_scores"].numpy()
-                    out["outliers"] = {sid: sc[i] for i, sid in enumerate(ids)}
-                else:
-                    out["outliers"] = None
+                out["outliers"] = ({sid: scores[i] for i, sid in enumerate(ids)}
+                                   if k >= 2 else None)
                 out["clusters"] = cluster_from_similarity(sim, ids, tau)
             return out
         finally:

@@ -20,30 +20,46 @@ from pathlib import Path
 import numpy as np
 
 from . import _native as N
-from .rasters import _PGM, RasterError, decode_surface_bytes
+from .rasters import RasterError, _Incomplete, _scan_pgm_header, decode_surface_bytes, pgm_header
 
-_HEAD = 512  # bytes read to parse a PGM header (comments included)
+_HEAD = 512  # first read for a header; long comment blocks fetch more
 
 
 def probe(source) -> tuple[int, int]:
     """(width, height) of a PGM/PNG file path or bytes without decoding the body."""
-    data = _head_bytes(source)
+    data = _head_bytes(source, 24)
     if data[:2] == b"P5":
-        m = _PGM.match(data)
-        if m is None:
-            raise RasterError("not a binary PGM (P5) file")
-        w, h, _ = (int(x) for x in m.groups())
+        w, h, _, _ = _pgm_head(source)
         return w, h
     if data[:8] == b"\x89PNG\r\n\x1a\n":
         return int.from_bytes(data[16:20], "big"), int.from_bytes(data[20:24], "big")
     raise RasterError("unrecognised surface format (expected PGM P5 or PNG)")
 
 
-def _head_bytes(source) -> bytes:
+def _head_bytes(source, n: int) -> bytes:
     if isinstance(source, (bytes, bytearray, memoryview)):
-        return bytes(source[:_HEAD])
+        return bytes(source[:n])
     with open(source, "rb") as f:
-        return f.read(_HEAD)
+        return f.read(n)
+
+
+def _pgm_head(source) -> tuple[int, int, int, int]:
+    """(width, height, maxval, body offset) of a PGM path or bytes: parse the first
+    _HEAD bytes, and read further (x64 each time, up to the whole file) while the header
+    is longer than what was read (e.g. long comment blocks)."""
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        return pgm_header(source)
+    n = _HEAD
+    size = os.path.getsize(source)
+    while True:
+        head = _head_bytes(source, n)
+        try:
+            _scan_pgm_header(head)
+            return pgm_header(head)
+        except _Incomplete:
+            if n >= size:
+                raise RasterError("not a binary PGM (P5) file") from None
+            n *= 64
 
 
 def decode_into(source, out: np.ndarray) -> tuple[int, int]:
@@ -52,24 +68,18 @@ def decode_into(source, out: np.ndarray) -> tuple[int, int]:
     if out.dtype != np.uint8 or not out.flags["C_CONTIGUOUS"]:
         raise ValueError("out must be a contiguous uint8 array")
     flat = out.reshape(-1)
-    head = _head_bytes(source)
-    if head[:2] == b"P5":
-        m = _PGM.match(head)
-        if m is None:
-            raise RasterError("not a binary PGM (P5) file")
-        w, h, maxval = (int(x) for x in m.groups())
-        if maxval > 255:
-            raise RasterError("16-bit PGM is not supported; maxval must be <= 255")
+    if _head_bytes(source, 2) == b"P5":
+        w, h, _, off = _pgm_head(source)
         if w * h != flat.size:
             raise RasterError(f"PGM is {w}x{h}, buffer holds {flat.size} px")
         if isinstance(source, (bytes, bytearray, memoryview)):
-            body = memoryview(source)[m.end():m.end() + w * h]
+            body = memoryview(source)[off:off + w * h]
             if len(body) < w * h:
                 raise RasterError(f"PGM truncated: expected {w * h} pixel bytes, got {len(body)}")
             flat[:] = np.frombuffer(body, dtype=np.uint8)
         else:
             with open(source, "rb") as f:
-                f.seek(m.end())
+                f.seek(off)
                 got = f.readinto(memoryview(flat))
             if got != w * h:
                 raise RasterError(f"PGM truncated: expected {w * h} pixel bytes, got {got}")

@@ -256,3 +256,25 @@ def test_bench_cli_fails_cleanly_without_gpu():
                         "--pixels", "4096", "--surfaces", "2", "--repeats", "1"],
                        capture_output=True, text=True, cwd=REPO, timeout=120)
     assert r.returncode == 2 and r.stderr.startswith("error:")
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_clustering_duplicate_ids_list_order(seed):
+    """Duplicate ids: clusters with the same first id keep the reference's list order
+    (smallest member index first, fs/analytics.py:220-226) — e.g. ids a b x x y with
+    sim(0,1)=.9, sim(1,3)=.85, sim(3,4)=.95 gives [[a, b], [x], [x, y]]."""
+    from paper_2104_14667_b200.analytics import cluster_from_similarity
+
+    ids = ["a", "b", "x", "x", "y"]
+    s = np.eye(5)
+    for i, j, v in [(0, 1, .9), (1, 3, .85), (3, 4, .95)]:
+        s[i, j] = s[j, i] = v
+    assert cluster_from_similarity(s, ids, 0.8) == [["a", "b"], ["x"], ["x", "y"]]
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 30))
+    x = np.round(rng.random((n, n)) * 5) / 5
+    s = np.minimum(x, x.T)
+    np.fill_diagonal(s, 1.0)
+    ids = [str(v) for v in rng.integers(0, max(2, n // 3), n)]
+    tau = float(rng.choice([0.2, 0.4, 0.6, 0.8]))
+    assert cluster_from_similarity(s, ids, tau) == O.cluster(s, ids, tau)
