@@ -1,26 +1,32 @@
 #!/usr/bin/env python
-"""Headline benchmark: ensemble Gpixels/s (incl. H2D) and FPS for 256 x 8192^2 masks.
+"""Headline benchmark: ensemble Gpixels/s incl. H2D, and FPS, for 256 x 8192^2 masks.
 
 Workload (BASELINE.json configs[1], "c2"): 256 flood-like masks of 8192 x 8192 uint8
-(17.18 GB).  One *step* = one full recompute of the working set:
-  overlap counts + overlap-class histogram + composite RGBA and the exact
-  pairwise-intersection Gram in ONE kernel over the bit-packed masks (tcgen05
-  kind::mxf4 + counter warps), the Jaccard matrix and outlier scores on the device, and
-  the complete-linkage clusters (tau 0.8) on the host.
+(17.18 GB) in PINNED host memory.  One *step* = one full frame through the public API:
+  H2D of every raster (2b-final dual-buffer DAG) overlapped with the binarize+pack
+  transform; ONE fused kernel for overlap counts + histogram + composite RGBA + the
+  exact pairwise-intersection Gram (tcgen05 kind::mxf4 + counter warps); Jaccard
+  matrix and outlier scores on the device; D2H of counts + RGBA + [bins | Gram] +
+  Jaccard + scores; complete-linkage clusters (tau 0.8) on the host.
 
-* ``value``: masks already resident (bit-packed) in HBM; unit Gpx/s = N*P / step time.
-* ``e2e``  : the same step through the public API from PINNED host rasters: every step
-  streams all 256 rasters (H2D, double-buffered, overlapped with the binarize+pack
-  transform), recomputes, and reads counts + RGBA + histogram + Gram back to the host.
-* ``--impl reference``: the reference's own CPU implementation (oracle/_ref = its
-  Cython accelerator compiled from its sources; else the oracle NumPy port) on all host
-  cores, on a bounded pixel window + pair sample, extrapolated to the workload.
+* ``value``: that end-to-end frame (host rasters in, host products out) over exactly
+  ``--steps`` timed steps: mask-pixels / s.  ``e2e`` repeats it with its byte counts.
+* ``resident``: the same recompute with the masks already bit-packed in HBM (the
+  interactive-recompute FPS of north_star), with the maps' D2H (``maps_to_host``) and
+  without (``device_only``).
+* ``roofline``: the dominant kernel of the recompute (the fused Gram+overlap kernel)
+  against the FP4 tensor peak; ``kernels`` adds the overlap pass and the transform
+  against HBM; ``e2e.roofline`` is the step against measured pinned PCIe H2D.
+* ``--impl reference``: the reference's own CPU implementation — the unmodified
+  reference package (baseline/_ref) run as shipped (single thread, numpy and cython
+  backends) and as an all-cores pixel-stripe harness around its unchanged primitives,
+  on the same workload; the all-cores number is the line's value.
 
-Multi-GPU (torchrun, one rank per GPU): the ensemble grows with N — 256 masks of
-8192 x (8192 N) px — and rank r owns rows [8192 r, 8192 (r+1)) of every mask, i.e. each
-GPU keeps exactly the 1-GPU workload (``scaling`` "weak", per-GPU work fixed).  The only
-exchange is the one NCCL all-reduce of the int64 [histogram | Gram] partials per frame;
-timings are the max over ranks and ``value`` = all masks' pixels / that time.
+Multi-GPU (torchrun, one rank per GPU): STRONG scaling by default — the fixed ensemble
+is cut into N row bands, rank r owns rows band(H, r, N) of every mask (one contiguous
+H2D per mask) and the only exchange is one NCCL all-reduce of the int64 [histogram |
+Gram] partials per frame; ``--scaling weak`` grows the raster to 8192 x 8192 N instead.
+Timings are the max over ranks; ``value`` = all masks' pixels / that time.
 """
 
 from __future__ import annotations
@@ -55,15 +61,19 @@ CONFIGS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong = the fixed ensemble in N row bands; weak = raster "
+                         "height grows with N (every rank keeps the 1-GPU workload)")
     ap.add_argument("--tau", type=float, default=0.8)
     ap.add_argument("--engine", default="tc-f4", choices=["tc-f4", "tc", "popc"])
-    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="profiling runs only: skip the end-to-end frames (value = resident)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--resident-steps", type=int, default=100)
     ap.add_argument("--band-rows", type=int, default=0, help="c4: rows per spatial band")
     ap.add_argument("--max-host-gb", type=float, default=0.0,
                     help="c4: cap on pinned host input per rank (0: 60%% of available RAM)")
@@ -175,112 +185,219 @@ def cpu_baseline(host_masks, width, height, k, window_px):
 
 
 # ---------------------------------------------------------------------------
-# reference arm
+# workload description shared by both arms (the driver compares the two config dicts)
 # ---------------------------------------------------------------------------
-def _ref_cells(task):
-    """The stripe's input rows for every mask (generation is untimed)."""
-    (lo, hi, k, width, height, seed, members, eps, _pairs) = task
-    from paper_2104_14667_b200.synth import synth_cells
+def workload_config(args, width, height, k, world) -> dict:
+    return {
+        "workload": (f"{args.config}: {k} flood-like masks {width}x{height} uint8 in host memory; "
+                     "one step = a full recompute frame: overlap counts + histogram + composite "
+                     "RGBA + pairwise Jaccard + outlier scores + complete-linkage clusters"),
+        "masks": k, "width": width, "height": height, "tau": args.tau,
+        "generator": "flood-like prototype+flip (fs_synth_host bytes), seed 2104",
+        "parallelism": (f"row-bands x{world}" if world > 1 else "single device"),
+        "l2": "every step reads all rasters from host memory (>> L2)",
+    }
 
-    return [synth_cells(width, height, i, seed=seed, members=members, eps=eps, row0=lo // width,
-                        rows=max(1, (hi - lo) // width), threads=1).reshape(-1)
-            for i in range(k)]
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation
+# ---------------------------------------------------------------------------
+def _load_reference_package():
+    """The unmodified reference package (pip-installed offline into baseline/_ref,
+    with its Cython accelerator built), or None when it is absent."""
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "floodstream").exists():
+        return None
+    sys.path.insert(0, str(ref))
+    import floodstream
+    import floodstream.analytics  # noqa: F401
+    import floodstream.backends  # noqa: F401
+
+    return floodstream
 
 
-def _ref_step(mod, cells, k, pairs):
-    """One timed pass of the reference primitives over a stripe of every mask."""
+def _primitive_modules(ref) -> dict:
+    """name -> the reference's primitive module (fs/backends.py:42-47); the oracle's
+    compiled copy of its _accel.pyx / its NumPy port when the package is absent."""
+    if ref is not None:
+        return dict(ref.backends.available_backends())
+    mods = {}
+    r = REPO / "oracle" / "_ref"
+    if any(r.glob("_accel*.so")):
+        sys.path.insert(0, str(r))
+        import _accel
+
+        mods["cython"] = _accel
+    from oracle import fs_oracle
+
+    mods["numpy"] = fs_oracle
+    return mods
+
+
+_REF = {}  # fork-inherited state of the all-cores harness (masks, module, pairs)
+
+
+def _stripe_worker(w, lo, hi, conn):
+    """One host core: the unchanged reference primitives on rows [lo, hi) of every mask,
+    one timed pass per "go" (fs/_kernels_np.py / fs/_accel.pyx, looped as
+    fs/analytics.py:118-181 does)."""
+    mod, masks, pairs, k = _REF["mod"], _REF["masks"], _REF["pairs"], _REF["k"]
+    cells = [m[lo:hi].reshape(-1) for m in masks]
     n = cells[0].size
-    t0 = time.perf_counter()
-    counts = np.zeros(n, dtype=np.uint32)
-    for c in cells:
-        mod.accumulate_into(counts, c)
-    mod.overlap_counts(counts, k)
-    out = np.zeros((n, 4), dtype=np.uint8)
-    mod.composite_fill(counts, k, out)
-    t1 = time.perf_counter()
-    for (i, j) in pairs:
-        mod.pair_counts(cells[i], cells[j])
-    t2 = time.perf_counter()
-    return n, t1 - t0, t2 - t1
-
-
-def _ref_server(task, conn):
-    """Persistent worker owning one stripe: generates it once, then runs one timed step
-    per "go" message (so steps measure only the reference kernels)."""
-    mod = _load_reference_kernels()
-    cells = _ref_cells(task)
-    k, pairs = task[2], task[8]
     while conn.recv() == "go":
-        conn.send(_ref_step(mod, cells, k, pairs))
+        t0 = time.perf_counter()
+        counts = np.zeros(n, dtype=np.uint32)
+        for c in cells:
+            mod.accumulate_into(counts, c)
+        mod.overlap_counts(counts, k)
+        out = np.zeros((n, 4), dtype=np.uint8)
+        mod.composite_fill(counts, k, out)
+        t1 = time.perf_counter()
+        for (i, j) in pairs:
+            mod.pair_counts(cells[i], cells[j])
+        t2 = time.perf_counter()
+        conn.send((n, t1 - t0, t2 - t1))
     conn.close()
 
 
-def _load_reference_kernels():
-    ref = REPO / "oracle" / "_ref"
-    if any(ref.glob("_accel*.so")):
-        sys.path.insert(0, str(ref))
-        import _accel  # the reference's Cython accelerator, compiled from its sources
-
-        return _accel
-    from oracle import fs_oracle  # the NumPy port of _kernels_np.py
-
-    return fs_oracle
+def _as_shipped_leg(ref, name, mod, surfaces, window_px, P, k, pairs, sim, tau):
+    """the reference's analytics, single thread, backend
+    `name`: per-pixel ops on a `window_px` window (scaled to P), Jaccard on the sampled
+    pairs (scaled to all pairs), outliers and clusters on the exact matrix
+    (similarity_matrix patched to return it, as §3.3 prescribes)."""
+    A = ref.analytics
+    saved = A.kernels
+    A.kernels = mod
+    try:
+        t = {}
+        t0 = time.perf_counter()
+        grid = A.accumulate(surfaces)
+        t["accumulate"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        A.overlap_histogram(grid)
+        t["overlap_histogram"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        A.composite_map(grid)
+        t["composite_map"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        for (i, j) in pairs:
+            A.jaccard(surfaces[i], surfaces[j])
+        t["jaccard_pairs"] = time.perf_counter() - t0
+        real_sim = A.similarity_matrix
+        A.similarity_matrix = lambda _s: sim
+        try:
+            t0 = time.perf_counter()
+            A.outlier_scores(surfaces)
+            t["outlier_scores"] = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            A.cluster_surfaces(surfaces, tau)
+            t["cluster_surfaces"] = time.perf_counter() - t0
+        finally:
+            A.similarity_matrix = real_sim
+    finally:
+        A.kernels = saved
+    npairs = k * (k - 1) // 2
+    px_scale = P / window_px
+    frame = ((t["accumulate"] + t["overlap_histogram"] + t["composite_map"]) * px_scale
+             + t["jaccard_pairs"] * px_scale * npairs / len(pairs)
+             + t["outlier_scores"] + t["cluster_surfaces"])
+    return {"backend": name, "threads": 1, "value": round(k * P / frame / 1e9, 6),
+            "unit": UNIT, "s_per_frame": round(frame, 3), "fps": round(1.0 / frame, 6),
+            "measured_s": {x: round(v, 4) for x, v in t.items()},
+            "window_px": window_px, "pairs": len(pairs),
+            "extrapolated": {"pixels": round(px_scale, 3),
+                             "pairs": round(npairs / len(pairs), 3)}}
 
 
 def reference_arm(args, width, height, k, members, eps, rank, world):
+    """The reference's own CPU implementation on the same workload and config.
+
+    * as shipped: the unmodified reference package, one thread, FLOODSTREAM_BACKEND
+      numpy and cython (BASELINE.md §3.3 item 3) — once, reported under ``as_shipped``;
+    * all cores (the line's value; §3.3 item 4): one process per host core, each
+      running the unchanged reference primitives of the faster as-shipped backend on
+      its stripe of rows of EVERY mask — the stripes tile the whole 8192 x 8192 raster,
+      so the per-pixel work is the full frame, measured — plus pair_counts of 64
+      sampled pairs on its stripe (summed over stripes = the full-raster pairs),
+      extrapolated to all k(k-1)/2 pairs; outliers and clusters run the reference's own
+      functions on the exact similarity matrix, timed once and added per step.
+    Under torchrun rank 0 alone runs; generation and the exact matrix are untimed."""
     if rank != 0:
         return None
-    height = height * world  # the same (weak-scaled) ensemble as the B200 arm
+    if args.scaling == "weak":
+        height = height * world
     import multiprocessing as mp
 
-    mod = _load_reference_kernels()
-    kind = "reference" if getattr(mod, "NAME", "") == "cython" else "port"
+    sys.path.insert(0, str(REPO / "tests"))
+    import oracle_c  # bench infrastructure: the exact Gram for the clustering input
+    from oracle import fs_oracle as O
+    from paper_2104_14667_b200.synth import synth_cells
+
+    ref = _load_reference_package()
+    mods = _primitive_modules(ref)
     cores = os.cpu_count() or 1
     P = width * height
-    # bounded sample per step: 8 rows of every mask per worker (large enough that the
-    # primitives' per-call overhead is negligible); the stripes are generated once, so
-    # a step costs only the timed reference kernels (~0.1-0.2 s) and even --steps 200
-    # finishes within a minute or two
-    rows_per_worker = 8
-    window_rows = rows_per_worker * cores
-    rng = np.random.default_rng(0)
     npairs_total = k * (k - 1) // 2
-    sample_pairs = [tuple(sorted(rng.choice(k, 2, replace=False).tolist())) for _ in range(8)]
-    tasks = [(w * rows_per_worker * width, (w + 1) * rows_per_worker * width, k, width, height,
-              2104, members, eps, sample_pairs) for w in range(cores)]
-    # clustering + outliers on an exact similarity matrix: the host logic of
-    # analytics.py:184-240, timed once (it does not depend on pixels)
-    from oracle import fs_oracle as O
-
-    sim = np.eye(k)
-    proto = np.arange(k) // members
-    sim = np.where(proto[:, None] == proto[None, :], 0.9, 0.3) + np.eye(k) * 0.1
+    # inputs (untimed): the full ensemble, generated with all host threads
+    masks = [synth_cells(width, height, i, seed=2104, members=members, eps=eps, threads=0)
+             for i in range(k)]
+    rng = np.random.default_rng(0)
+    pairs = []
+    while len(pairs) < min(64, npairs_total):
+        i, j = sorted(rng.choice(k, 2, replace=False).tolist())
+        if (i, j) not in pairs:
+            pairs.append((i, j))
     ids = [f"s{i:04d}" for i in range(k)]
-    t0 = time.perf_counter()
-    O.outlier_scores(sim, ids)
-    O.cluster(sim, ids, args.tau)
-    t_host = time.perf_counter() - t0
-    times = []
+    sim = O.similarity_from_gram(oracle_c.gram([m.reshape(-1) for m in masks], cores))
+
+    # ---- as shipped: single thread, both backends --------------------------------
+    as_shipped = {}
+    if ref is not None:
+        rows_w = min(height, max(1, -(-(16 << 20) // width)))  # >= 16 Mpx window
+        surfaces = [ref.RasterSurface(id=ids[i], name=ids[i], width=width, height=rows_w,
+                                      cells=masks[i][:rows_w]) for i in range(k)]
+        for name in ("numpy", "cython"):
+            if name in mods:
+                as_shipped[name] = _as_shipped_leg(ref, name, mods[name], surfaces,
+                                                   rows_w * width, P, k, pairs, sim, args.tau)
+        del surfaces
+    # host analytics per frame (outliers + clusters on the exact matrix)
+    if as_shipped:
+        best = min(as_shipped.values(), key=lambda r: r["s_per_frame"])
+        harness_backend = best["backend"]
+        t_host = best["measured_s"]["outlier_scores"] + best["measured_s"]["cluster_surfaces"]
+    else:
+        harness_backend = "cython" if "cython" in mods else "numpy"
+        t0 = time.perf_counter()
+        O.outlier_scores(sim, ids)
+        O.cluster(sim, ids, args.tau)
+        t_host = time.perf_counter() - t0
+
+    # ---- all cores: pixel stripes over every mask ----------------------------------
+    _REF.update(mod=mods[harness_backend], masks=masks, pairs=pairs, k=k)
+    nw = min(cores, height)
+    bounds = [(w * height // nw, (w + 1) * height // nw) for w in range(nw)]
     ctx = mp.get_context("fork")
     conns, procs = [], []
-    for task in tasks:
+    for w, (lo, hi) in enumerate(bounds):
         parent, child = ctx.Pipe()
-        proc = ctx.Process(target=_ref_server, args=(task, child), daemon=True)
+        proc = ctx.Process(target=_stripe_worker, args=(w, lo, hi, child), daemon=True)
         proc.start()
         conns.append(parent)
         procs.append(proc)
+    times, samples = [], []
     try:
         for step in range(args.warmup + args.steps):
             for c in conns:
                 c.send("go")
             res = [c.recv() for c in conns]
-            n_win = sum(r[0] for r in res)
+            assert sum(r[0] for r in res) == P  # the stripes tile the raster
             t_pix = max(r[1] for r in res)
             t_pair = max(r[2] for r in res)
-            scale = P / n_win
-            t_step = t_pix * scale + t_pair * scale * (npairs_total / len(sample_pairs)) + t_host
+            t_step = t_pix + t_pair * (npairs_total / len(pairs)) + t_host
             if step >= args.warmup:
                 times.append(t_step)
+                samples.append(t_pix + t_pair + t_host)
     finally:
         for c in conns:
             try:
@@ -291,23 +408,31 @@ def reference_arm(args, width, height, k, members, eps, rank, world):
             proc.join(timeout=10)
     t = statistics.median(times)
     value = k * P / t / 1e9
+    kind = "reference" if ref is not None or harness_backend == "cython" else "port"
+    src = ("baseline/_ref floodstream (unmodified reference package)" if ref is not None else
+           "oracle/_ref (reference _accel.pyx compiled from its sources)"
+           if harness_backend == "cython" else "oracle NumPy port")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {k} masks {width}x{height}"
-                               + (f" ({world} x {height // world}-row bands)" if world > 1 else ""),
-                   "tau": args.tau},
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": workload_config(args, width, height, k, world),
         "fps": round(1.0 / t, 6),
+        "extrapolated": {"sample_s": round(statistics.median(samples), 4),
+                         "scale": {"pixels": 1.0, "pairs": round(npairs_total / len(pairs), 3)},
+                         "note": "per-pixel ops measured on the full raster (stripes of all "
+                                 f"{nw} workers tile it); pair_counts measured on {len(pairs)} "
+                                 "sampled pairs and scaled to all pairs"},
         "cpu_baseline": {
-            "value": round(value, 6), "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": (f"{'oracle/_ref (reference _accel.pyx)' if kind == 'reference' else 'oracle NumPy port'}"
-                       f" accumulate_into/overlap_counts/composite_fill on {window_rows} rows x "
-                       f"{k} masks split over {cores} processes, pair_counts on "
-                       f"{len(sample_pairs)} sampled pairs, scaled to {P} px and "
-                       f"{npairs_total} pairs; + clustering/outliers {t_host:.2f} s (exact sim)"),
+            "value": round(value, 6), "unit": UNIT, "cores": nw, "kind": kind,
+            "sample": (f"{src}, {harness_backend} primitives: accumulate_into x{k} + "
+                       f"overlap_counts + composite_fill on {nw} row stripes tiling all "
+                       f"{height} rows, pair_counts on {len(pairs)} sampled pairs scaled "
+                       f"to {npairs_total}; + outlier_scores/cluster_surfaces "
+                       f"{t_host:.2f} s on the exact matrix"),
         },
+        "as_shipped": as_shipped or None,
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -447,16 +572,13 @@ def bench_banded(args, width, height, k, members, eps, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per_step * 1e3, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
-            "config": {"workload": f"c4: {k} flood-like masks {width}x{height} uint8 streamed "
-                                   f"in spatial bands of {band_rows} rows from pinned host "
-                                   "memory (H2D + transform + recompute + D2H of maps per step)",
-                       "masks": k, "width": width, "height": height, "tau": args.tau,
-                       "rows_per_rank": rows, "rows_total": total_rows,
-                       "sampled": (f"host RAM holds {rows} of {row_band(height, rank, world)[1]}"
-                                   " rows per rank; value counts only the streamed rows")
-                       if sampled else None,
-                       "parallelism": f"row blocks x{world}" if world > 1 else "single GPU",
-                       "l2": "every step streams all rasters from host memory (>> L2)"},
+            "config": workload_config(args, width, height, k, world),
+            "setup": {"band_rows": band_rows, "rows_per_rank": rows, "rows_total": total_rows,
+                      "sampled": (f"host RAM holds {rows} of {row_band(height, rank, world)[1]}"
+                                  " rows per rank; value counts only the streamed rows")
+                      if sampled else None,
+                      "path": "spatial bands streamed from pinned host memory (H2D + transform "
+                              "+ recompute + D2H of maps per step)"},
             "fps": round(args.steps / t, 4),
             "bands": st.bands,
             "roofline": {"bound": "pcie_h2d", "achieved": round(h2d / per_step / 1e9, 2),
@@ -510,7 +632,7 @@ def main():
 
     from paper_2104_14667_b200 import _native as N
     from paper_2104_14667_b200.dist import ShardedEnsemble
-    from paper_2104_14667_b200.synth import synth_cells, synth_cells_gpu
+    from paper_2104_14667_b200.synth import synth_cells_gpu
 
     gpu, backend = dist_setup(local_rank, world)
     torch.cuda.set_device(gpu)
@@ -524,8 +646,8 @@ def main():
         else:
             dist.init_process_group(backend)
     dev = torch.device("cuda", gpu)
-    band_h = height
-    height = height * world  # weak scaling: every rank keeps a full 1-GPU band
+    if args.scaling == "weak":
+        height = height * world  # every rank keeps a full 1-GPU band
     P = width * height
     slots = list(range(k))
     ids = [f"s{i:04d}" for i in range(k)]
@@ -537,7 +659,6 @@ def main():
     depth = 3 if k <= 256 else 6
     P_band = rows * width
     ens = sh.ens
-    ens.synth(0, k, seed=2104, members=members, eps=eps)
     stream = sh.stream
 
     def barrier():
@@ -553,91 +674,119 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    kern = {"overlap": [], "gram": [], "recompute": []}
+    def sum_over_ranks(x: int) -> int:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        return int(t.item())
 
-    def sample_kernels(_f):
-        # CUDA-event duration of the previous frame's recompute call (ensemble stream)
-        if _f > 0:
-            kern["recompute"].append(ens.kernel_ms("recompute"))
+    def timed_frames(n, **kw):
+        """n pipelined frames between CUDA events on the ensemble stream (after a
+        barrier), max over ranks; the events bracket every frame's device work and,
+        because run_frames returns only after the last frame's products reached the
+        host, its D2H too."""
+        if n <= 0:
+            return 0.0, 0.0, None
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        w0 = time.perf_counter()
+        out = sh.run_frames(slots, n, tau=args.tau, engine=args.engine, ids=ids, keep=False,
+                            depth=depth, analytics_ranks="root", **kw)
+        e1.record(stream)
+        e1.synchronize()
+        wall = time.perf_counter() - w0
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / 1e3), max_over_ranks(wall), out[-1]
 
-    # ---- resident timed region: K pipelined full recomputes ---------------------------
-    sh.run_frames(slots, args.warmup, tau=args.tau, engine=args.engine, ids=ids,
-                  analytics_ranks="root", keep=False, depth=depth)
-    barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    # ---- pinned host rasters: this rank's rows of every mask (generated, untimed) ----
+    host = None
+    if not args.no_e2e:
+        host = [N.PinnedBuffer((P_band,)) for _ in range(k)]
+        for i in range(k):
+            synth_cells_gpu(width, height, i, seed=2104, members=members, eps=eps, row0=row0,
+                            rows=rows, out=host[i].array.reshape(rows, width))
+        arrays = [h.array for h in host]
+    else:
+        ens.synth(0, k, seed=2104, members=members, eps=eps)
+
+    def upload(_f):
+        ens.stream(arrays, variant="2b-final", already_banded=True)
+
+    # ---- the metric: K end-to-end frames (host rasters in, host products out) ----
+    clocks = None
+    n_clusters = None
+    if not args.no_e2e:
+        timed_frames(args.warmup, maps_to_host=True, before_frame=upload)
+        with Clocks(gpu) as clk:
+            t_e2e, wall_e2e, last = timed_frames(args.steps, maps_to_host=True,
+                                                 before_frame=upload)
+        clocks = clk.summary()
+        if rank == 0:
+            n_clusters = len(last["clusters"])
+        kern_pack = ens.kernel_ms("pack")
+    # ---- resident recompute: masks bit-packed in HBM (interactive FPS) ------------
+    rsteps = max(args.resident_steps, 1)
+    timed_frames(args.warmup)
+    with Clocks(gpu) as clk_r:
+        t_res, wall_res, last_r = timed_frames(rsteps)
+    t_res_maps, _, _ = timed_frames(max(rsteps // 4, 1), maps_to_host=True)
+    if clocks is None:
+        clocks = clk_r.summary()
+        n_clusters = len(last_r["clusters"]) if rank == 0 else None
     host_ms = []
-    with Clocks(gpu) as clk:
-        barrier()
-        ev0.record(stream)
-        t_wall0 = time.perf_counter()
-        last = sh.run_frames(slots, args.steps, tau=args.tau, engine=args.engine, ids=ids,
-                             analytics_ranks="root", keep=False, depth=depth)
-        ev1.record(stream)
-        ev1.synchronize()
-        t_wall = time.perf_counter() - t_wall0
-        barrier()
-    t_res = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
-    clocks = clk.summary()
-    ms_step = t_res / args.steps * 1e3
-    value = k * P * args.steps / t_res / 1e9
-    if rank == 0:  # host part of a frame (the complete-linkage merge loop), timed apart;
-        # Jaccard and outlier scores are computed on the device inside the frame
+    if rank == 0:  # host part of a frame (the complete-linkage merge loop), timed apart
         from paper_2104_14667_b200.analytics import cluster_from_similarity
 
-        sim_last = last[0]["similarity"]
         for _ in range(3):
             t0 = time.perf_counter()
-            n_clusters = len(cluster_from_similarity(sim_last, ids, args.tau))
+            cluster_from_similarity(last_r["similarity"], ids, args.tau)
             host_ms.append((time.perf_counter() - t0) * 1e3)
 
-    # ---- per-kernel roofline: CUDA-event durations on the ensemble stream, sampled in
-    # extra untimed frames (reading them blocks, which would break the pipelining) ----
-    sh.run_frames(slots, 6, tau=args.tau, engine=args.engine, ids=ids, analytics_ranks="none",
-                  keep=False, before_frame=sample_kernels, depth=depth)
-    sample_kernels(1)
-    fused = None
-    # the two stages as separate kernels (the unfused path), for the breakdown
+    # ---- per-kernel rooflines: CUDA-event durations on the ensemble stream, sampled
+    # in extra untimed calls (reading them blocks, which would break the pipelining) ----
+    kern = {"overlap": [], "gram": [], "recompute": []}
     d_c = torch.empty(P_band, dtype=torch.int32, device=dev)
     d_r = torch.empty(P_band * 4, dtype=torch.uint8, device=dev)
     d_b = torch.empty(k + 1, dtype=torch.int64, device=dev)
     d_g = torch.empty(k * k, dtype=torch.int64, device=dev)
+    fused = None
     for _ in range(6):
+        fused = ens.products(slots, engine=args.engine, out_counts=d_c.data_ptr(),
+                             out_rgba=d_r.data_ptr(), out_bins=d_b.data_ptr(),
+                             out_gram=d_g.data_ptr(), device_outputs=True)[4]
+        kern["recompute"].append(ens.kernel_ms("recompute"))
         ens.overlap(slots, out_counts=d_c.data_ptr(), out_rgba=d_r.data_ptr(),
                     out_bins=d_b.data_ptr(), device_outputs=True)
         kern["overlap"].append(ens.kernel_ms("overlap"))
         ens.gram(slots, engine=args.engine, out=d_g.data_ptr(), device_outputs=True)
         kern["gram"].append(ens.kernel_ms("gram"))
-        fused = ens.products(slots, engine=args.engine, out_counts=d_c.data_ptr(),
-                             out_rgba=d_r.data_ptr(), out_bins=d_b.data_ptr(),
-                             out_gram=d_g.data_ptr(), device_outputs=True)[4]
     del d_c, d_r, d_b, d_g
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     traffic = load_traffic()
     ov_ms = statistics.median(kern["overlap"])
     gr_ms = statistics.median(kern["gram"])
+    rc_ms = statistics.median(kern["recompute"])
     ov_bytes = k * P_band / 8 + 4 * P_band + 4 * P_band + 8 * (k + 1)
     gram_ops = float(k) * (k + 1) * P_band  # upper triangle incl. diagonal, MAC = 2 ops
-    # dense tensor peaks (B200_PROFILING.md fallback table; MEASURED_PEAKS.json has bf16 only)
-    t_peak, t_kind = {"tc-f4": (9000.0, "fp4 (kind::mxf4) 9 PFLOP/s dense"),
-                      "tc": (4500.0, "int8 (kind::i8) 4.5 POPS dense"),
-                      "popc": (4500.0, "int8 4.5 POPS dense (CUDA-core engine, for scale)")}[args.engine]
+    t_peak, t_kind = tensor_peak(args.engine)
     rl_over = {"bound": "hbm", "achieved": round(ov_bytes / ov_ms / 1e6, 1), "peak": hbm,
                "unit": "GB/s", "frac": round(ov_bytes / ov_ms / 1e6 / hbm, 4),
                "traffic": traffic.get("k_overlap"), "kernel_ms": round(ov_ms, 4),
                "bytes_per_launch": int(ov_bytes),
                "bytes_def": "N*P/8 packed read + 4P counts + 4P RGBA + 8(N+1) bins",
                "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy test)"}
+    ops_def = ("N(N+1)*P = 2 ops x the N(N+1)/2 distinct mask pairs x P px (the kernel "
+               "issues 3/4 N^2 P MACs: 128-row MMA granularity)")
     rl_gram = {"bound": "tensor", "achieved": round(gram_ops / gr_ms / 1e9, 1), "peak": t_peak,
                "unit": "TFLOP/s", "frac": round(gram_ops / gr_ms / 1e9 / t_peak, 4),
                "traffic": traffic.get("k_gram_tc_f4" if args.engine == "tc-f4" else "k_gram_tc"),
-               "kernel_ms": round(gr_ms, 4), "ops_per_launch": gram_ops,
-               "ops_def": "N(N+1)*P = 2 ops x the N(N+1)/2 distinct mask pairs x P px "
-                          "(the kernel issues 3/4 N^2 P MACs: 128-row MMA granularity)",
+               "kernel_ms": round(gr_ms, 4), "ops_per_launch": gram_ops, "ops_def": ops_def,
                "peak_note": t_kind}
-    rc_ms = statistics.median(kern["recompute"])
     npanels_k = -(-k // (128 if k <= 128 else 256))
+    one_panel = bool(fused) and npanels_k == 1
     rl_fused = {"bound": "tensor",
                 "kernel": ("k_gram_tc<...,FUSE> + k_gram_reduce" if npanels_k == 1 else
                            "k_gram_tc<...,FUSE> (partial counts) + k_gram_pair_f4 + "
@@ -646,38 +795,24 @@ def main():
                 "fused": bool(fused), "achieved": round(gram_ops / rc_ms / 1e9, 1),
                 "peak": t_peak, "unit": "TFLOP/s",
                 "frac": round(gram_ops / rc_ms / 1e9 / t_peak, 4),
-                "traffic": traffic.get("k_gram_tc_fused") if (fused and npanels_k == 1) else None,
-                # tensor-pipe utilisation of this kernel from the committed ncu capture
-                "ncu": traffic.get("k_gram_tc_fused_ncu") if (fused and npanels_k == 1) else None,
-                "kernel_ms": round(rc_ms, 4), "ops_per_launch": gram_ops,
-                "ops_def": rl_gram["ops_def"], "peak_note": t_kind,
+                "traffic": traffic.get("k_gram_tc_fused") if one_panel else None,
+                "ncu": traffic.get("k_gram_tc_fused_ncu") if one_panel else None,
+                "kernel_ms": round(rc_ms, 4), "ops_per_launch": gram_ops, "ops_def": ops_def,
+                "peak_note": t_kind,
                 "hbm_achieved_gbs": round(ov_bytes / rc_ms / 1e6, 1),
                 "hbm_frac": round(ov_bytes / rc_ms / 1e6 / hbm, 4),
                 "hbm_bytes_def": "same algorithmic bytes as the overlap pass (the Gram reads "
                                  "the same packed tiles)"}
-    if fused and args.engine == "tc-f4" and k > 128 and npanels_k == 1:
-        # What actually limits the fused kernel: shared-memory bandwidth (128 B/clk/SM).
-        # Per 256-px K stage of the 256-mask diagonal panel the MMAs read 80 KB of
-        # operands (rows 0-127 x N=256 and rows 128-255 x N=128, 4 K-steps), TMA writes
-        # 8 KB of raw bits, the expanders read them and write 32 KB of e2m1 operands,
-        # and the counter warps read the same 8 KB; the MMAs alone need 768 cycles.
-        clk_hz = float((clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
-        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-        stages = -(-P_band // 1024) * 4 / nsm
-        smem_ms = stages * (136 * 1024 / 128) / clk_hz * 1e3
-        mma_ms = stages * 768 / clk_hz * 1e3
-        rl_fused["limiter_model"] = {
-            "limiter": "smem", "smem_bytes_per_stage": 136 * 1024, "smem_bytes_per_clk": 128,
-            "mma_cycles_per_stage": 768, "stages_per_sm": round(stages, 1),
-            "smem_bound_ms": round(smem_ms, 4), "mma_bound_ms": round(mma_ms, 4),
-            "frac_of_smem_bound": round(smem_ms / rc_ms, 4),
-            "note": "no binary tcgen05 kind: 1-bit masks are expanded to e2m1 in SMEM and "
-                    "kind::mxf4 reads both operands from SMEM (no TMEM-A form)",
-            # the kernel rebuilt without each part in turn (FS_PROBE_* builds): skeleton
-            # (TMA ring + stage handoffs) 0.53 ms, + expansion 0.67, + counting 0.87,
-            # + MMAs 1.08 at C2; TMA alone streams the same boxes at 7.25 TB/s
-            "part_isolation": "profiles/r3f/parts.txt"}
-    dominant = rl_fused
+    kernels = {"recompute": rl_fused, "overlap": rl_over, "gram": rl_gram}
+    if not args.no_e2e:
+        tx_bytes = P_band + P_band / 8
+        kernels["transform"] = {
+            "bound": "hbm", "kernel": "k_pack_vec (binarize + bit-pack one raster)",
+            "achieved": round(tx_bytes / kern_pack / 1e6, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(tx_bytes / kern_pack / 1e6 / hbm, 4), "kernel_ms": round(kern_pack, 4),
+            "bytes_per_launch": int(tx_bytes), "bytes_def": "P raw read + P/8 packed write",
+            "launches_per_step": k, "traffic": traffic.get("k_pack_vec_c2_raster")
+            if (P_band == 8192 * 8192) else None}
 
     # ---- the same frames through the native C++ loop (single device, informational) ----
     native = None
@@ -686,107 +821,85 @@ def main():
             pipe.run(args.warmup)
             torch.cuda.synchronize()
             t0n = time.perf_counter()
-            rn = pipe.run(args.steps)
+            rn = pipe.run(rsteps)
             wall_n = time.perf_counter() - t0n
-        native = {"ms_per_step": round(rn["device_ms"] / args.steps, 4),
-                  "fps": round(args.steps / (rn["device_ms"] / 1e3), 3),
-                  "wall_ms_per_step": round(wall_n / args.steps * 1e3, 4),
+        native = {"ms_per_step": round(rn["device_ms"] / rsteps, 4),
+                  "fps": round(rsteps / (rn["device_ms"] / 1e3), 3),
+                  "wall_ms_per_step": round(wall_n / rsteps * 1e3, 4),
                   "clusters": len(rn["clusters"]),
                   "path": "fs_pipeline_run: recompute + device Jaccard/outliers + D2H queued "
                           "while C++ workers run the linkage (no Python per frame)"}
 
-    # ---- end-to-end through the public API from pinned host rasters --------------------
-    e2e = None
-    host = h_counts = None
-    if not args.no_e2e:
-        host = [N.PinnedBuffer((P_band,)) for _ in range(k)]
-        for i in range(k):  # the generator's bytes, produced on the GPU (fs_synth_gpu)
-            synth_cells_gpu(width, height, i, seed=2104, members=members, eps=eps, row0=row0,
-                            rows=rows, out=host[i].array.reshape(rows, width))
-        arrays = [h.array for h in host]
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and host is not None:
+        cpu = cpu_baseline([b.array for b in host], width, rows, k, min(P_band, 1 << 22))
 
-        def upload(_f):
-            ens.stream(arrays, variant="2b-final", already_banded=True)
-
-        sh.run_frames(slots, 1, tau=args.tau, engine=args.engine, ids=ids, maps_to_host=True,
-                      analytics_ranks="root", keep=False, depth=depth, before_frame=upload)  # warm-up
-        barrier()
-        ev0.record(stream)
-        res = sh.run_frames(slots, args.e2e_steps, tau=args.tau, engine=args.engine, ids=ids,
-                            maps_to_host=True, analytics_ranks="root", keep=False, depth=depth,
-                            before_frame=upload)
-        ev1.record(stream)
-        ev1.synchronize()
-        barrier()
-        t_e2e = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
-        h2d = int(k * P_band)
-        pcie = pcie_h2d_gbs()
-        t_min = h2d / (pcie * 1e9)
-        e2e = {"value": round(k * P * args.e2e_steps / t_e2e / 1e9, 4), "unit": UNIT,
-               "h2d_bytes_per_step": int(k * P),
+    px_total = k * sum_over_ranks(P_band)
+    res = {"value": round(px_total * rsteps / t_res / 1e9, 3), "unit": UNIT,
+           "ms_per_step": round(t_res / rsteps * 1e3, 4), "fps": round(rsteps / t_res, 3),
+           "steps": rsteps, "wall_ms_per_step": round(wall_res / rsteps * 1e3, 4),
+           "path": "device_only: fused recompute + all-reduce + device Jaccard/outliers + D2H "
+                   "of [bins | Gram] + Jaccard + scores, host linkage overlapped",
+           "maps_to_host": {"ms_per_step": round(t_res_maps / max(rsteps // 4, 1) * 1e3, 4),
+                            "fps": round(max(rsteps // 4, 1) / t_res_maps, 3),
+                            "d2h_bytes_per_step": int(8 * P_band),
+                            "path": "the same + counts and RGBA maps to pinned host memory"},
+           "native_pipeline": native}
+    if rank != 0:
+        torch.cuda.synchronize()
+        sh.close()
+        if host is not None:
+            for b in host:
+                b.free()
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    pcie = pcie_h2d_gbs()
+    config = workload_config(args, width, height, k, world)
+    setup = {"gram_engine": args.engine, "rows_per_rank": rows,
+             "pipelining": f"{depth} frames in flight: host analytics of frame f overlap "
+                           "device work of frame f+1",
+             "value_kind": "end to end: pinned host rasters in, host products out"}
+    if args.no_e2e:
+        value, ms_step, fps, e2e = res["value"], res["ms_per_step"], res["fps"], None
+        setup["value_kind"] = "resident (--no-e2e profiling run, not the metric)"
+    else:
+        value = px_total * args.steps / t_e2e / 1e9
+        ms_step = t_e2e / args.steps * 1e3
+        fps = args.steps / t_e2e
+        h2d_rank = k * P_band
+        t_min = h2d_rank / (pcie * 1e9)
+        e2e = {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": int(px_total),
                # counts + RGBA of every band, and per rank [bins | Gram] + Jaccard + scores
                "d2h_bytes_per_step": int(8 * P + world * 8 * ((k + 1) + 2 * k * k + k)),
-               "ms_per_step": round(t_e2e / args.e2e_steps * 1e3, 3),
-               "fps": round(args.e2e_steps / t_e2e, 4), "steps": args.e2e_steps,
-               "roofline": {"bound": "pcie_h2d", "achieved": round(h2d / (t_e2e / args.e2e_steps) / 1e9, 2),
+               "ms_per_step": round(ms_step, 3), "fps": round(fps, 4), "steps": args.steps,
+               "wall_ms_per_step": round(wall_e2e / args.steps * 1e3, 3),
+               "roofline": {"bound": "pcie_h2d",
+                            "achieved": round(h2d_rank / (t_e2e / args.steps) / 1e9, 2),
                             "peak": round(pcie, 2), "unit": "GB/s",
-                            "frac": round(t_min / (t_e2e / args.e2e_steps), 4),
+                            "frac": round(t_min / (t_e2e / args.steps), 4),
                             "peak_note": "measured pinned H2D, 1 GiB copy, best of 5"},
-               "path": "DeviceEnsemble.stream(2b-final, pinned) -> overlap -> gram -> D2H "
-                       "counts+RGBA+bins+Gram -> Jaccard/outliers/clusters"}
-        h_counts = res[-1].get("counts")
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        src = [b.array for b in host] if host is not None else [
-            synth_cells(width, height, i, seed=2104, members=members, eps=eps, rows=256)
-            for i in range(k)]
-        window = min(P, 1 << 22, src[0].size)
-        cpu = cpu_baseline(src, width, height, k, window)
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {k} flood-like masks {width}x{height} uint8 "
-                                   "(bit-packed resident in HBM), full recompute per step"
-                                   + (f"; {world} row bands of {band_h} rows, one per GPU"
-                                      if world > 1 else ""),
-                       "masks": k, "width": width, "height": height, "tau": args.tau,
-                       "gram_engine": args.engine,
-                       "parallelism": f"row-bands x{world}" if world > 1 else "single GPU",
-                       "l2": f"inputs (bit-packed {k * P_band / 8 / 1e9:.2f} GB per GPU) larger "
-                             "than L2; no flush",
-                       "pipelining": "double-buffered frames: host analytics of frame f "
-                                     "overlap device work of frame f+1"},
-            "fps": round(args.steps / t_res, 3),
-            "wall_ms_per_step": round(t_wall / args.steps * 1e3, 4),
-            "host_linkage_ms": round(statistics.median(host_ms), 4) if host_ms else None,
-            "native_pipeline": native,
-            "clusters": n_clusters if host_ms else None,
-            "roofline": dominant,
-            "kernels": {"recompute": rl_fused, "overlap": rl_over, "gram": rl_gram},
-            "clocks": clocks,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "gpu_launches": None,
-        }
-        # our kernels per resident step: fused overlap (1) + Gram
-        if args.engine in ("tc", "tc-f4"):
-            npanels = -(-k // (128 if k <= 128 else 256))
-            gram_launches = 1 + (1 if npanels > 1 else 0) + 1  # diag, off-diag, reduce
-        else:
-            gram_launches = 1 + (1 if k > 64 else 0)  # popc, mirror
-        # + the overlap kernel unless fused into the diagonal Gram CTAs (beyond one panel
-        # the fused path adds a combine kernel instead)
-        # + Jaccard and outlier kernels on the summed Gram
-        analytic_launches = 2 if k >= 2 else 1
-        npan = -(-k // (128 if k <= 128 else 256))
-        line["gpu_launches"] = (gram_launches + (0 if (fused and npan == 1) else 1)
-                                + analytic_launches) * args.steps
-        print(json.dumps(line), flush=True)
+               "path": "pinned host rasters -> DeviceEnsemble.stream (2b-final) -> fused "
+                       "recompute -> D2H counts+RGBA+[bins|Gram]+Jaccard+scores -> clusters"}
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic", "config": config, "setup": setup,
+        "fps": round(fps, 4), "resident": res,
+        "host_linkage_ms": round(statistics.median(host_ms), 4) if host_ms else None,
+        "clusters": n_clusters,
+        "roofline": rl_fused, "kernels": kernels, "clocks": clocks, "e2e": e2e,
+        "cpu_baseline": cpu, "gpu_launches": None,
+    }
+    # our kernels per e2e step: k transform launches + the recompute + Jaccard/outliers
+    if args.engine in ("tc", "tc-f4"):
+        gram_launches = 1 + (1 if npanels_k > 1 else 0) + 1  # diag, off-diag, reduce
+    else:
+        gram_launches = 1 + (1 if k > 64 else 0)  # popc, mirror
+    per_step = gram_launches + (0 if one_panel else 1) + (2 if k >= 2 else 1)
+    line["gpu_launches"] = (per_step + (0 if args.no_e2e else k)) * args.steps
+    print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
     sh.close()
     if host is not None:
@@ -794,6 +907,26 @@ def main():
             b.free()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def tensor_peak(engine: str) -> tuple[float, str]:
+    """Dense tensor peak for the Gram's kind: the builder-measured FP4 / int8 MMA rate
+    (profiles/tensor_peaks.json, tools/probes/mma_probe.cu) when present, else the
+    B200_PROFILING.md nominal figure; the note says which."""
+    meas = {}
+    p = REPO / "profiles" / "tensor_peaks.json"
+    if p.exists():
+        try:
+            meas = json.loads(p.read_text())
+        except Exception:
+            meas = {}
+    key = {"tc-f4": "fp4_tflops", "tc": "int8_tops", "popc": "int8_tops"}[engine]
+    nominal = {"tc-f4": 9000.0, "tc": 4500.0, "popc": 4500.0}[engine]
+    kind = {"tc-f4": "fp4 (kind::mxf4)", "tc": "int8 (kind::i8)",
+            "popc": "int8 (kind::i8), CUDA-core engine shown for scale"}[engine]
+    if meas.get(key):
+        return float(meas[key]), f"{kind} {meas[key]:.0f} TFLOP/s dense, measured ({p.name})"
+    return nominal, f"{kind} {nominal:.0f} TFLOP/s dense, nominal (B200_PROFILING.md)"
 
 
 if __name__ == "__main__":
