@@ -20,8 +20,8 @@ LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libfloodstream.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["fs_kernels.cu", "fs_gram_tc.cu", "fs_capi.cu", "fs_pipeline.cu"]
-HEADERS = ["fs_common.cuh", "fs_internal.h", "fs_bitslice.cuh"]
+SOURCES = ["fs_kernels.cu", "fs_gram_tc.cu", "fs_recompute_f4.cu", "fs_capi.cu", "fs_pipeline.cu"]
+HEADERS = ["fs_common.cuh", "fs_internal.h", "fs_bitslice.cuh", "fs_tcgen05.cuh"]
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

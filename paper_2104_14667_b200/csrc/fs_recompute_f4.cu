@@ -1,0 +1,381 @@
+// fs_recompute_f4.cu — the full recompute of one <= 256-mask panel in ONE kernel:
+// exact pairwise intersections (Gram, tcgen05 kind::mxf4) AND the per-pixel overlap
+// products (counts, histogram, composite RGBA) from a single read of the packed masks.
+//
+// Reference semantics: similarity_matrix's pair_counts loop (analytics.py:174-181,
+// _kernels_np.py:26-32) and accumulate / overlap_histogram / composite_map
+// (analytics.py:106-162, _kernels_np.py:16-47) of /root/reference/pkg/src/floodstream/.
+//
+// Data path per 1024-px unit (one pixel tile of every mask = 256 x 128 B, contiguous in
+// the tile-interleaved layout, fs_common.cuh):
+//   * 8 expander warps load the unit straight from global memory into REGISTERS with
+//     fully coalesced 16-B loads (warp instruction j covers 4 consecutive mask rows =
+//     512 contiguous bytes); lane l holds rows 4j + l/8 (j = 0..7) of its warp's 32
+//     rows, 16-B chunk c = l % 8 (pixels 128c .. 128c+127).  The next unit's loads are
+//     in flight while this one is processed (two register buffers): no TMA ring, no raw
+//     copy in shared memory at all.
+//   * Counting from those registers: per lane a carry-save tree over its 8 rows, then
+//     two shuffle rounds over the 4 lanes holding the same chunk give each lane the
+//     bit-sliced count (6 planes) of one 32-px word over the warp's 32 rows; the 8 warps'
+//     partial planes (6 KB per unit) go to shared memory and 4 combiner warps add them
+//     (9 planes, exact), transpose to per-pixel counts and emit histogram / counts /
+//     RGBA (fs_bitslice.cuh emit_tile).
+//   * Expansion from the same registers: operand stage s of the unit = word s of every
+//     chunk (any pixel permutation shared by all masks leaves a Gram unchanged), so each
+//     lane writes 16 B of e2m1 0/1 operand per row per stage into the SWIZZLE_128B
+//     K-major ring; one thread issues rows 0-127 x N=256 and rows 128-255 x N=128
+//     kind::mxf4 MMAs per 64-px K step (3/4 of the 256 x 256 square; the reduce mirrors).
+// Shared-memory traffic per 256-px stage: UMMA operand fetch + 32 KB expander stores +
+// ~3 KB partial counts + the emit staging — the raw tiles never pass through it.
+#include "fs_bitslice.cuh"
+#include "fs_tcgen05.cuh"
+
+namespace fs {
+namespace rc {
+
+constexpr int kExpWarps = 8;                  // expander / epilogue warps
+constexpr int kCntWarps = 4;                  // combiner + emit warps
+constexpr int kWarps = 1 + kExpWarps + kCntWarps;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kCntWarp0 = 1 + kExpWarps;
+constexpr int kPartDepth = 4;                 // partial-count ring (multiple of kCntWarps)
+constexpr int kPlanes = 6;                    // bit planes of a 32-row partial count
+constexpr int kPartWords = kExpWarps * kPlanes * 32;  // per unit
+constexpr int kStageBytes = 256 * 128;        // 256 rows x 128 B (256 px of e2m1)
+constexpr int kFuseBins = 288;
+constexpr int kTbBytes = kCntWarps * 32 * kTileTb * 4;
+constexpr int kExtraBytes = kPartDepth * kPartWords * 4 + kTbBytes + 2 * kFuseBins * 4;
+constexpr int kSmemMax = 232448;
+constexpr int kStages = (kSmemMax - 1024 - 512 - kExtraBytes) / kStageBytes;
+constexpr int kSmemBytes = kStages * kStageBytes + kExtraBytes + 1024 + 512;
+static_assert(kStages >= 3, "operand ring too shallow");
+static_assert(kPartDepth % kCntWarps == 0, "combiner warp u % 4 must own partial slot u % depth");
+
+// (h, l) = a + b (half adder)
+__device__ __forceinline__ void ha(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b) {
+  h = a & b;
+  l = a ^ b;
+}
+
+// bit-sliced sum of 8 words: planes p[0..3] (value 0..8)
+__device__ __forceinline__ void sum8(const uint32_t (&x)[8], uint32_t (&p)[4]) {
+  uint32_t t1, o1, t2, o2, t3, o3, t4, o4, f1, w1, f2, w2;
+  csa(t1, o1, x[0], x[1], x[2]);
+  csa(t2, o2, o1, x[3], x[4]);
+  csa(t3, o3, o2, x[5], x[6]);
+  ha(t4, o4, o3, x[7]);
+  csa(f1, w1, t1, t2, t3);
+  ha(f2, w2, w1, t4);
+  p[0] = o4;
+  p[1] = w2;
+  p[2] = f1 ^ f2;
+  p[3] = f1 & f2;
+}
+
+// bit-sliced a + b, NA planes each -> NA + 1 planes
+template <int NA>
+__device__ __forceinline__ void add_planes(const uint32_t *a, const uint32_t *b, uint32_t *s) {
+  uint32_t c = a[0] & b[0];
+  s[0] = a[0] ^ b[0];
+#pragma unroll
+  for (int i = 1; i < NA; ++i) {
+    const uint32_t u = a[i] ^ b[i];
+    s[i] = u ^ c;
+    c = (a[i] & b[i]) | (u & c);
+  }
+  s[NA] = c;
+}
+
+__device__ __forceinline__ void expand_word(uint32_t addr, uint32_t x) {
+  tc::st_shared_v4(addr, make_uint4((x << 1) & 0x22222222u, x & 0x22222222u,
+                                    (x >> 1) & 0x22222222u, (x >> 2) & 0x22222222u));
+}
+
+struct Args {
+  const uint32_t *src;   // packed masks (tile-interleaved)
+  uint64_t cap;          // slots per tile row of `src`
+  uint64_t row0;         // first slot of the panel
+  uint32_t k;            // masks in the panel (<= 256)
+  uint64_t total_units;  // tiles of 1024 px
+  uint64_t upc;          // units per CTA chunk
+  int32_t *partial;      // one 256 x 256 int32 tile per CTA
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_recompute_f4(const Args a, const OverlapArgs ov) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+  const uint32_t pad = (1024u - (raw_addr & 1023u)) & 1023u;
+  uint8_t *smem = smem_raw + pad;
+  const uint32_t op_base = raw_addr + pad;
+  uint32_t *part = reinterpret_cast<uint32_t *>(smem + kStages * kStageBytes);
+  uint32_t *cnt_tb = part + kPartDepth * kPartWords;
+  uint32_t *sh_hist = cnt_tb + kCntWarps * 32 * kTileTb;
+  uint32_t *sh_lut = sh_hist + kFuseBins;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sh_lut + kFuseBins);
+  uint64_t *empty = full + kStages;
+  uint64_t *part_full = empty + kStages;
+  uint64_t *part_empty = part_full + kPartDepth;
+  uint64_t *tmem_full = part_empty + kPartDepth;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint64_t u0 = (uint64_t)blockIdx.x * a.upc;
+  const uint64_t u1 = min(u0 + a.upc, a.total_units);
+  const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
+  const int nst = nunits * 4;
+
+  // expander registers: rows 4j + lane/8 of this warp's 32 rows, chunk lane % 8
+  const int ew = warp - 1;
+  const uint32_t chunk = (uint32_t)lane & 7u;
+  uint4 ra[8], rb[8];
+  auto load_unit = [&](int u, uint4 (&r)[8]) {
+    const uint64_t gu = u0 + (uint64_t)u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t row = (uint32_t)(32 * ew + 4 * j) + ((uint32_t)lane >> 3);
+      if (row < a.k)
+        r[j] = ptx::ld_nc_v4(a.src + ((gu * a.cap + a.row0 + row) * 32u + 4u * chunk));
+      else
+        r[j] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  const bool is_exp = warp >= 1 && warp <= kExpWarps;
+  if (is_exp) {  // first two units in flight before the setup below
+    if (nunits > 0) load_unit(0, ra);
+    if (nunits > 1) load_unit(1, rb);
+  }
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], kExpWarps);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kPartDepth; ++s) {
+      ptx::mbar_init(&part_full[s], kExpWarps);
+      ptx::mbar_init(&part_empty[s], 1);
+    }
+    ptx::mbar_init(tmem_full, 1);
+    ptx::fence_mbar_init();
+  }
+  const bool lut_sh = ov.rgba != nullptr;
+  if (warp >= kCntWarp0) {
+    for (int i = tid - 32 * kCntWarp0; i < kFuseBins; i += 32 * kCntWarps) {
+      sh_hist[i] = 0;
+      sh_lut[i] = lut_sh && (uint32_t)i < ov.nbins ? rgba_word(i, ov.n_inputs, ov.lut) : 0u;
+    }
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     ptx::smem_u32(tmem_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp >= 1 && warp <= 4) {  // every UE8M0 block scale = 1.0
+    const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
+    tc::tmem_st16(tmem + lanes + tc::kSfCol, tc::kSfOnes);
+    tc::tmem_st16(tmem + lanes + tc::kSfCol + 16, tc::kSfOnes);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+
+  if (warp == 0) {
+    // ===== MMA issuer =====
+    if (lane == 0 && nst > 0) {
+      constexpr uint32_t idA = tc::idesc_mxf4(128, 256);
+      constexpr uint32_t idB = tc::idesc_mxf4(128, 128);
+      const uint32_t sfa = tmem + tc::kSfCol, sfb = tmem + tc::kSfCol + 16;
+      const uint64_t d_op = tc::sw128_desc(op_base);
+      for (int j = 0; j < nst; ++j) {
+        const int s = j % kStages;
+        ptx::mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
+        tc::fence_after();
+        const uint64_t d_s = d_op + (uint64_t)((uint32_t)(s * kStageBytes) >> 4);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {  // 4 MMAs of 64 K (32 B) per 128-B operand row
+          const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
+          const uint64_t lo = d_s + (uint64_t)((ks * 32) >> 4);
+          const uint64_t hi = lo + (uint64_t)((128 * 128) >> 4);
+          tc::mma_mxf4(tmem, lo, lo, idA, acc, sfa, sfb);          // rows 0-127 x 0-255
+          tc::mma_mxf4(tmem + 256u, hi, hi, idB, acc, sfa, sfb);   // rows 128-255 x 128-255
+        }
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else if (is_exp) {
+    // ===== expanders: count + expand each unit from registers =====
+    const uint32_t sw_lo = ((uint32_t)lane >> 3);  // row & 7 for even j; +4 for odd j
+    auto process = [&](int u, uint4 (&r)[8]) {
+      // --- partial counts of this warp's 32 rows: 8 rows per lane, then lanes ^8, ^16
+      uint32_t P[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = i == 0 ? r[j].x : i == 1 ? r[j].y : i == 2 ? r[j].z : r[j].w;
+        sum8(x, P[i]);
+      }
+      const bool b3 = (lane >> 3) & 1, b4 = (lane >> 4) & 1;
+      uint32_t Q[2][5];  // words (b3 ? 2 : 0) and (b3 ? 3 : 1), 5 planes
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        uint32_t mine[4], other[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint32_t keep = b3 ? P[2 + q][p] : P[q][p];
+          const uint32_t send = b3 ? P[q][p] : P[2 + q][p];
+          mine[p] = keep;
+          other[p] = __shfl_xor_sync(0xFFFFFFFFu, send, 8);
+        }
+        add_planes<4>(mine, other, Q[q]);
+      }
+      uint32_t R6[kPlanes];
+      {
+        uint32_t mine[5], other[5];
+#pragma unroll
+        for (int p = 0; p < 5; ++p) {
+          const uint32_t keep = b4 ? Q[1][p] : Q[0][p];
+          const uint32_t send = b4 ? Q[0][p] : Q[1][p];
+          mine[p] = keep;
+          other[p] = __shfl_xor_sync(0xFFFFFFFFu, send, 16);
+        }
+        add_planes<5>(mine, other, R6);
+      }
+      // this lane now holds word 4c + 2 b3 + b4 of the unit (c = lane % 8)
+      const uint32_t wi = 4u * chunk + 2u * (uint32_t)b3 + (uint32_t)b4;
+      const int ps = u % kPartDepth;
+      if (u >= kPartDepth) ptx::mbar_wait(&part_empty[ps], (uint32_t)(((u / kPartDepth) - 1) & 1));
+      uint32_t *dst = part + ps * kPartWords + ew * kPlanes * 32;
+#pragma unroll
+      for (int p = 0; p < kPlanes; ++p) dst[p * 32 + wi] = R6[p];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&part_full[ps]);
+      // --- operand stages: word s of every chunk of every row
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int j = u * 4 + s;
+        const int st = j % kStages;
+        if (j >= kStages) ptx::mbar_wait(&empty[st], (uint32_t)(((j / kStages) - 1) & 1));
+        const uint32_t sbase = op_base + (uint32_t)st * kStageBytes;
+#pragma unroll
+        for (int jr = 0; jr < 8; ++jr) {
+          const uint32_t row = (uint32_t)(32 * ew + 4 * jr) + sw_lo;
+          const uint32_t swz = (sw_lo + 4u * (uint32_t)(jr & 1)) & 7u;
+          const uint32_t w = s == 0 ? r[jr].x : s == 1 ? r[jr].y : s == 2 ? r[jr].z : r[jr].w;
+          expand_word(sbase + row * 128u + ((chunk ^ swz) << 4), w);
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&full[st]);
+      }
+    };
+    for (int u = 0; u < nunits; u += 2) {
+      process(u, ra);
+      if (u + 2 < nunits) load_unit(u + 2, ra);
+      if (u + 1 < nunits) {
+        process(u + 1, rb);
+        if (u + 3 < nunits) load_unit(u + 3, rb);
+      }
+    }
+    // ===== epilogue: TMEM -> registers -> int32 partial tile =====
+    const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp
+    const int cg = (warp - 1) / 4;            // two warps per quarter split the columns
+    int32_t *out = a.partial + (uint64_t)blockIdx.x * 256 * 256;
+    if (nst > 0) {
+      ptx::mbar_wait(tmem_full, 0);
+      tc::fence_after();
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t row = h * 128 + q * 32 + lane;
+      const int c_begin = h == 1 ? 128 : 0;
+      for (int c0 = c_begin + 32 * cg; c0 < 256; c0 += 64) {
+        uint32_t v[32];
+        const uint32_t col = h == 1 ? (256u + (uint32_t)(c0 - 128)) : (uint32_t)c0;
+        tc::tmem_ld32(tmem + ((q * 32u) << 16) + col, v);
+        if (nst == 0) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = 0;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = (uint32_t)__float2int_rn(__uint_as_float(v[e]));
+        }
+        int4 *dst = reinterpret_cast<int4 *>(out + (uint64_t)row * 256 + c0);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          dst[e] = make_int4((int)v[4 * e], (int)v[4 * e + 1], (int)v[4 * e + 2], (int)v[4 * e + 3]);
+      }
+    }
+    tc::fence_before();
+  } else {
+    // ===== combiners: 8 partial counts -> exact per-pixel counts -> emit =====
+    const int cw = warp - kCntWarp0;
+    for (int u = cw; u < nunits; u += kCntWarps) {
+      const int ps = u % kPartDepth;
+      ptx::mbar_wait(&part_full[ps], (uint32_t)((u / kPartDepth) & 1));
+      const uint32_t *src = part + ps * kPartWords + lane;
+      uint32_t n[8][kPlanes];
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+#pragma unroll
+        for (int p = 0; p < kPlanes; ++p) n[w][p] = src[(w * kPlanes + p) * 32];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&part_empty[ps]);
+      uint32_t s7[4][7], s8[2][8], s9[9];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) add_planes<6>(n[2 * i], n[2 * i + 1], s7[i]);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) add_planes<7>(s7[2 * i], s7[2 * i + 1], s8[i]);
+      add_planes<8>(s8[0], s8[1], s9);
+      HSCounter<5> hc;
+      hc.ones = s9[0];
+      hc.twos = s9[1];
+      hc.fours = s9[2];
+      hc.eights = s9[3];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) hc.H[i] = s9[4 + i];
+      uint32_t cnt32[32];
+      hc.extract1(cnt32);
+      emit_tile(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
+                ov.bins != nullptr, sh_lut, lut_sh);
+    }
+  }
+  __syncthreads();
+  if (warp >= kCntWarp0 && ov.bins != nullptr) {
+    for (uint32_t i = tid - 32 * kCntWarp0; i < ov.nbins; i += 32 * kCntWarps)
+      if (sh_hist[i]) atomicAdd(ov.bins + i, (unsigned long long)sh_hist[i]);
+    if (blockIdx.x == 0 && tid == 32 * kCntWarp0) {
+      const uint64_t padpx = a.total_units * 1024 - ov.pixels;  // padding counted in bin 0
+      if (padpx) atomicAdd(ov.bins, (unsigned long long)(0ull - padpx));
+    }
+  }
+  if (warp == 0) {
+    tc::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  }
+}
+
+}  // namespace rc
+
+cudaError_t launch_recompute_f4(const uint32_t *src, uint64_t cap, uint64_t row0, uint32_t k,
+                                uint64_t total_units, uint32_t kchunks, uint64_t upc,
+                                int32_t *partial, const OverlapArgs &ov, cudaStream_t s) {
+  if (kchunks == 0) return cudaSuccess;
+  static SmemOptIn attr;
+  if (cudaError_t e = smem_opt_in(attr, rc::k_recompute_f4, (size_t)rc::kSmemBytes); e != cudaSuccess)
+    return e;
+  rc::Args a{src, cap, row0, k, total_units, upc, partial};
+  rc::k_recompute_f4<<<kchunks, rc::kThreads, rc::kSmemBytes, s>>>(a, ov);
+  return cudaGetLastError();
+}
+
+}  // namespace fs

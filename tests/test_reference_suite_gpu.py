@@ -71,5 +71,5 @@ def test_reference_streaming_suite_with_streaming_bound():
     assert summary["binding"]["floodstream.streaming"] == "paper_2104_14667_b200.streaming"
     unexpected = [f for f in summary["failed"] if f not in summary["cost_model_failed"]]
     assert not unexpected, (unexpected, r.stdout[-3000:])
-    assert summary["files"]["test_streaming.py"]["passed"] >= 20
+    assert summary["files"]["test_streaming.py"]["passed"] >= 19  # 28 tests, 9 listed
     assert summary["files"]["test_service.py"]["passed"] > 0
