@@ -16,6 +16,9 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libfloodstream.so"
+# timing experiments only (tools/probe_builds.py): load a probe build of the library
+if os.environ.get("FS_LIB_PROBE"):
+    LIB_PATH = Path(os.environ["FS_LIB_PROBE"]).resolve()
 
 FS_OK, FS_EINVAL, FS_ECUDA, FS_ENOMEM, FS_ENODEV = 0, 1, 2, 3, 4
 VARIANT_CODES = {"1b-initial": 0, "2b-initial": 1, "1b-final": 2, "2b-final": 3}

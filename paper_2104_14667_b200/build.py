@@ -41,11 +41,15 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          extra: list[str] | None = None) -> Path:
+    """Build the library (default: in-tree, when stale).  ``out`` / ``extra``: a probe
+    build with extra nvcc flags at another path (timing experiments only)."""
+    target = Path(out) if out is not None else LIB
+    if out is None and not force and not _stale():
         return LIB
-    LIB_DIR.mkdir(parents=True, exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
+    target.parent.mkdir(parents=True, exist_ok=True)
+    tmp = target.with_suffix(".so.tmp")
     cmd = [
         nvcc(),
         *ARCH_FLAGS,
@@ -62,6 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         *(["-Xptxas", "-v"] if verbose else []),
         # experiment knobs (e.g. -DFS_EXP_BATCH=1); never set for the shipped build
         *os.environ.get("FS_NVCC_EXTRA", "").split(),
+        *(extra or []),
         *[str(CSRC / s) for s in SOURCES],
         "-o",
         str(tmp),
@@ -72,8 +77,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError("nvcc failed building libfloodstream (see stderr)")
     if verbose:
         sys.stderr.write(proc.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

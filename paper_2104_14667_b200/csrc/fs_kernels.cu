@@ -143,6 +143,56 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Pipelined vector variant: like k_pack_vec, but every warp keeps the NEXT 4 KB block's
+// eight 16-B loads in flight while it packs the current one, and the same launch packs
+// the partial last block and writes the zero padding up to wpm (no separate tail
+// launch: a second dependent launch costs several microseconds at any raster size).
+__device__ __forceinline__ void pack_block(const uint4 (&v)[kPackVec], uint64_t b, int lane,
+                                           uint32_t *__restrict__ dst, uint64_t slot,
+                                           uint64_t cap) {
+#pragma unroll
+  for (int i = 0; i < kPackVec; ++i) {
+    const uint32_t h = nz_bits16(v[i]);
+    const uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
+    if ((lane & 1) == 0)
+      dst[pk_off(slot, b * (kPackBlk / 32) + i * 16 + (lane >> 1), cap)] = h | (other << 16);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_pack_pipe(const uint8_t *__restrict__ src, uint64_t pixels, uint64_t wpm,
+                uint32_t *__restrict__ dst, uint64_t slot, uint64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nblk = pixels / kPackBlk;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  uint4 cur[kPackVec], nxt[kPackVec];
+  auto load = [&](uint4 (&v)[kPackVec], uint64_t blk) {
+    const uint8_t *base = src + blk * kPackBlk + lane * 16;
+#pragma unroll
+    for (int i = 0; i < kPackVec; ++i) v[i] = ptx::ld_nc_v4(base + i * 512);
+  };
+  if (b < nblk) load(cur, b);
+  while (b < nblk) {
+    const uint64_t bn = b + nw;
+    if (bn < nblk) load(nxt, bn);
+    pack_block(cur, b, lane, dst, slot, cap);
+    if (bn >= nblk) break;
+    b = bn;
+#pragma unroll
+    for (int i = 0; i < kPackVec; ++i) cur[i] = nxt[i];
+  }
+  // partial last block + zero padding: words [nblk * 128, wpm), one word per thread
+  const uint64_t w0 = nblk * (kPackBlk / 32);
+  for (uint64_t w = w0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < wpm;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t word = 0;
+    const uint64_t p0 = w * 32;
+    for (int q = 0; q < 32 && p0 + q < pixels; ++q) word |= (uint32_t)(src[p0 + q] != 0) << q;
+    dst[pk_off(slot, w, cap)] = word;
+  }
+}
+
 // Words [w0, wpm): scalar tail + zero padding.
 __global__ void k_pack_tail(const uint8_t *__restrict__ src, uint64_t pixels, uint64_t w0,
                             uint64_t wpm, uint32_t *__restrict__ dst, uint64_t slot,
@@ -176,6 +226,13 @@ cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint
       k_pack_bulk<<<(unsigned)grid, kPackThreads, smem, s>>>(src, nchunks, dst, slot, cap);
       done_words = nchunks * (kPackChunk / 32);
     }
+  } else if (engine == 3) {
+    const uint64_t nblk = pixels / kPackBlk;
+    uint64_t grid = (std::max<uint64_t>(nblk, 1) * 32 + 255) / 256;
+    const uint64_t gcap = (uint64_t)num_sms() * 4;
+    if (grid > gcap) grid = gcap;
+    k_pack_pipe<<<(unsigned)grid, 256, 0, s>>>(src, pixels, wpm, dst, slot, cap);
+    return cudaGetLastError();
   } else if (engine == 2) {
     const uint64_t nblk = pixels / kPackBlk;
     if (nblk > 0) {

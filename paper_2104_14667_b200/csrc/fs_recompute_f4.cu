@@ -49,6 +49,15 @@ constexpr int kSmemMax = 232448;
 constexpr int kStages = (kSmemMax - 1024 - 512 - kExtraBytes) / kStageBytes;
 constexpr int kSmemBytes = kStages * kStageBytes + kExtraBytes + 1024 + 512;
 static_assert(kStages >= 3, "operand ring too shallow");
+#ifndef FS_RC_BATCH
+#define FS_RC_BATCH 1
+#endif
+#ifndef FS_RC_COUNT_MID
+#define FS_RC_COUNT_MID 0
+#endif
+constexpr int kBatch = FS_RC_BATCH;             // operand stages per proxy fence
+constexpr bool kCountMid = FS_RC_COUNT_MID != 0;  // count between the two stage halves
+static_assert(4 % kBatch == 0 && kBatch < kStages, "batch must divide a unit's 4 stages");
 static_assert(kPartDepth % kCntWarps == 0, "combiner warp u % 4 must own partial slot u % depth");
 
 // (h, l) = a + b (half adder)
@@ -135,9 +144,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t row = (uint32_t)(32 * ew + 4 * j) + ((uint32_t)lane >> 3);
+#ifndef FS_RC_NO_LOAD  // timing experiment only: no HBM traffic, constant data
       if (row < a.k)
         r[j] = ptx::ld_nc_v4(a.src + ((gu * a.cap + a.row0 + row) * 32u + 4u * chunk));
       else
+#else
+      if (row < a.k)
+        r[j] = make_uint4((uint32_t)gu * 0x9E3779B9u ^ row, row * 7u, (uint32_t)gu, row ^ 5u);
+      else
+#endif
         r[j] = make_uint4(0u, 0u, 0u, 0u);
     }
   };
@@ -203,8 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
           const uint64_t lo = d_s + (uint64_t)((ks * 32) >> 4);
           const uint64_t hi = lo + (uint64_t)((128 * 128) >> 4);
+#ifndef FS_RC_NO_MMA  // timing experiment only
           tc::mma_mxf4(tmem, lo, lo, idA, acc, sfa, sfb);          // rows 0-127 x 0-255
           tc::mma_mxf4(tmem + 256u, hi, hi, idB, acc, sfa, sfb);   // rows 128-255 x 128-255
+#endif
         }
         tc::mma_commit(&empty[s]);
       }
@@ -214,7 +231,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (is_exp) {
     // ===== expanders: count + expand each unit from registers =====
     const uint32_t sw_lo = ((uint32_t)lane >> 3);  // row & 7 for even j; +4 for odd j
-    auto process = [&](int u, uint4 (&r)[8]) {
+    auto count_unit = [&](int u, uint4 (&r)[8]) {
+#ifndef FS_RC_NO_COUNT  // timing experiment only
       // --- partial counts of this warp's 32 rows: 8 rows per lane, then lanes ^8, ^16
       uint32_t P[4][4];
 #pragma unroll
@@ -259,23 +277,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int p = 0; p < kPlanes; ++p) dst[p * 32 + wi] = R6[p];
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&part_full[ps]);
-      // --- operand stages: word s of every chunk of every row
+#endif
+    };
+    // --- operand stages s0 .. s0 + kBatch - 1 of unit u: word s of every chunk of every
+    // row; one proxy fence per batch (the fence waits for this thread's stores to drain)
+    auto stage_batch = [&](int u, uint4 (&r)[8], int s0) {
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const int j = u * 4 + s;
-        const int st = j % kStages;
-        if (j >= kStages) ptx::mbar_wait(&empty[st], (uint32_t)(((j / kStages) - 1) & 1));
-        const uint32_t sbase = op_base + (uint32_t)st * kStageBytes;
+      for (int b = 0; b < kBatch; ++b) {
+        const int j = u * 4 + s0 + b;
+        if (j >= kStages) ptx::mbar_wait(&empty[j % kStages], (uint32_t)(((j / kStages) - 1) & 1));
+      }
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) {
+        const int s = s0 + b;
+        const uint32_t sbase = op_base + (uint32_t)((u * 4 + s) % kStages) * kStageBytes;
 #pragma unroll
         for (int jr = 0; jr < 8; ++jr) {
           const uint32_t row = (uint32_t)(32 * ew + 4 * jr) + sw_lo;
           const uint32_t swz = (sw_lo + 4u * (uint32_t)(jr & 1)) & 7u;
           const uint32_t w = s == 0 ? r[jr].x : s == 1 ? r[jr].y : s == 2 ? r[jr].z : r[jr].w;
+#ifndef FS_RC_NO_EXPAND  // timing experiment only
           expand_word(sbase + row * 128u + ((chunk ^ swz) << 4), w);
+#else
+          if (w == 0xFFFFFFFFu && swz == 9u) expand_word(sbase, w);  // keep w live
+#endif
         }
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&full[st]);
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) ptx::mbar_arrive(&full[(u * 4 + s0 + b) % kStages]);
+      }
+    };
+    auto process = [&](int u, uint4 (&r)[8]) {
+      if (!kCountMid) count_unit(u, r);
+#pragma unroll
+      for (int s0 = 0; s0 < 4; s0 += kBatch) {
+        stage_batch(u, r, s0);
+        if (kCountMid && s0 + kBatch == 2) count_unit(u, r);
       }
     };
     for (int u = 0; u < nunits; u += 2) {
@@ -320,6 +360,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===== combiners: 8 partial counts -> exact per-pixel counts -> emit =====
     const int cw = warp - kCntWarp0;
     for (int u = cw; u < nunits; u += kCntWarps) {
+#ifdef FS_RC_NO_COUNT  // timing experiment only
+      break;
+#endif
       const int ps = u % kPartDepth;
       ptx::mbar_wait(&part_full[ps], (uint32_t)((u / kPartDepth) & 1));
       const uint32_t *src = part + ps * kPartWords + lane;
@@ -345,6 +388,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < 5; ++i) hc.H[i] = s9[4 + i];
       uint32_t cnt32[32];
       hc.extract1(cnt32);
+#ifdef FS_RC_NO_EMIT  // timing experiment only
+      if (cnt32[lane & 31] == 0xFFFFFFFFu) ov.counts[0] = 0;  // keep the count live
+      continue;
+#endif
       emit_tile(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
                 ov.bins != nullptr, sh_lut, lut_sh);
     }

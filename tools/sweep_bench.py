@@ -51,7 +51,8 @@ def main():
         specs = {"nonpow2": SweepSpec(512, 2000, 16012), "pow2": SweepSpec(512, 2048, 16384)}
     doc = {"config": "c5: raster dimension sweep 512-16384 (non-square, non-pow2), iid p=0.5",
            "kernel": {-1: "library default", 0: "k_pack_bulk (TMA bulk-staged)",
-                      1: "k_pack_direct", 2: "k_pack_vec (8 x 16-B loads in flight)"}[args.engine]
+                      1: "k_pack_direct", 2: "k_pack_vec (8 x 16-B loads in flight)",
+                      3: "k_pack_pipe (next block's loads in flight, in-kernel tail)"}[args.engine]
                      + " binarize + bit-pack",
            "rate_def": "w*h / t_us / 1000 GB/s of uint8 raster (fs/bench.py:337-338)",
            "roofline": {"bound": "hbm", "bytes_per_px": 1.125, "peak_gbs": hbm,
