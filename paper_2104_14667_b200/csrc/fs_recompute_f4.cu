@@ -50,15 +50,38 @@ constexpr int kStages = (kSmemMax - 1024 - 512 - kExtraBytes) / kStageBytes;
 constexpr int kSmemBytes = kStages * kStageBytes + kExtraBytes + 1024 + 512;
 static_assert(kStages >= 3, "operand ring too shallow");
 #ifndef FS_RC_BATCH
-#define FS_RC_BATCH 1
+#define FS_RC_BATCH 2
 #endif
 #ifndef FS_RC_COUNT_MID
 #define FS_RC_COUNT_MID 0
+#endif
+// L2 prefetch distance in units: while unit u is processed, one lane bulk-prefetches unit
+// u + d (cp.async.bulk.prefetch.L2, the unit's k rows x 128 B are contiguous) so the
+// register loads issued two units ahead hit L2 (0 = off)
+#ifndef FS_RC_L2PF
+#define FS_RC_L2PF 4
+#endif
+// L2 policy of the prefetched units: 1 = evict_last, 0 = default
+#ifndef FS_RC_PF_HINT
+#define FS_RC_PF_HINT 0
 #endif
 constexpr int kBatch = FS_RC_BATCH;             // operand stages per proxy fence
 constexpr bool kCountMid = FS_RC_COUNT_MID != 0;  // count between the two stage halves
 static_assert(4 % kBatch == 0 && kBatch < kStages, "batch must divide a unit's 4 stages");
 static_assert(kPartDepth % kCntWarps == 0, "combiner warp u % 4 must own partial slot u % depth");
+
+// bulk L2 prefetch of one unit (k rows x 128 B, contiguous)
+__device__ __forceinline__ void l2_prefetch(const void *p, uint32_t bytes) {
+#if FS_RC_PF_HINT
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes),
+               "l"(pol)
+               : "memory");
+#else
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+#endif
+}
 
 // (h, l) = a + b (half adder)
 __device__ __forceinline__ void ha(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b) {
@@ -311,6 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     auto process = [&](int u, uint4 (&r)[8]) {
+#if FS_RC_L2PF > 0
+      if (ew == 0 && lane == 0 && u + FS_RC_L2PF < nunits)
+        l2_prefetch(a.src + ((u0 + (uint64_t)(u + FS_RC_L2PF)) * a.cap + a.row0) * 32u, a.k * 128u);
+#endif
       if (!kCountMid) count_unit(u, r);
 #pragma unroll
       for (int s0 = 0; s0 < 4; s0 += kBatch) {

@@ -1,0 +1,159 @@
+// tc_peak.cu — measured dense tensor-core peaks on one B200 for the two Gram kinds this
+// package uses (kind::mxf4 and kind::i8), the denominators of bench.py's tensor roofline.
+//
+// One CTA per SM; one thread streams `iters` x 4 back-to-back tcgen05.mma M=128 N=256
+// (K = 64 e2m1 / 32 int8 per instruction) from a zero-filled SMEM operand into TMEM, then
+// one commit.  The kernel is timed with CUDA events (best of `reps`), so the figure is
+// what the chip sustains at its own clock, not a cycles x nominal-clock product.
+// "same" reuses one 128-row operand as A and B (no operand-fetch limit); "distinct" reads
+// A and a separate 256-row B (the fetch-bound case).  Prints one JSON object; the
+// fp4_tflops / int8_tops keys feed profiles/tensor_peaks.json.
+//
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tc_peak tc_peak.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t a) {
+  uint64_t d = 0;
+  d |= (uint64_t)((a >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+// kind::mxf4: e2m1 A/B, UE8M0 scales, f32 accumulate
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) |
+         ((uint32_t)(M >> 4) << 24);
+}
+// kind::i8: u8 A/B (format 0, as the library's Gram), s32 accumulate (D format 2)
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+template <bool FP4>
+__global__ void __launch_bounds__(128, 1) k_peak(int iters, int distinct) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t done_bar;
+  __shared__ uint32_t tslot;
+  const uint32_t base = (smem_u32(sm) + 1023u) & ~1023u;
+  for (int i = threadIdx.x; i < (48 * 1024) / 16; i += blockDim.x)
+    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(base + 16 * i), "r"(0));
+  if (threadIdx.x == 0) mbar_init(&done_bar, 1);
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tslot;
+  if (FP4) {  // block scales = 1.0 (UE8M0 0x7F) in columns 448..479
+    const uint32_t lanes = (uint32_t)((threadIdx.x >> 5) * 32) << 16;
+    const uint32_t v = 0x7F7F7F7Fu;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1};" ::"r"(tmem + lanes + 448u),
+        "r"(v));
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1};" ::"r"(tmem + lanes + 464u),
+        "r"(v));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (threadIdx.x == 0) {
+    const uint32_t id = FP4 ? idesc_mxf4(128, 256) : idesc_i8(128, 256);
+    const uint32_t sfa = tmem + 448u, sfb = tmem + 464u;
+    const uint32_t a_base = base, b_base = distinct ? base + 16 * 1024 : base;
+    for (int j = 0; j < iters; ++j) {
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint64_t da = sw128_desc(a_base + ks * 32), db = sw128_desc(b_base + ks * 32);
+        const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
+        if (FP4)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], "
+              "[%6], p;\n\t}" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(id), "r"(acc), "r"(sfa), "r"(sfb));
+        else
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(id), "r"(acc));
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+        smem_u32(&done_bar)));
+    mbar_wait(&done_bar, 0);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <bool FP4>
+static double run(int sms, int iters, int distinct, int reps) {
+  const int smem = 64 * 1024;
+  cudaFuncSetAttribute(k_peak<FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_peak<FP4><<<sms, 128, smem>>>(iters / 8, distinct);  // warm-up (clocks up)
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(a);
+    k_peak<FP4><<<sms, 128, smem>>>(iters, distinct);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  const double k_per = FP4 ? 64.0 : 32.0;
+  const double ops = 2.0 * 128 * 256 * k_per * 4.0 * iters * sms;
+  return ops / (best * 1e-3) / 1e12;
+}
+
+int main() {
+  int sms = 0, dev = 0, clk = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  const int iters = 1 << 16, reps = 5;
+  const double f4s = run<true>(sms, iters, 0, reps), f4d = run<true>(sms, iters, 1, reps);
+  const double i8s = run<false>(sms, iters, 0, reps), i8d = run<false>(sms, iters, 1, reps);
+  const cudaError_t e = cudaDeviceSynchronize();
+  printf("{\"probe\": \"tcgen05.mma M=128 N=256 back to back, one CTA per SM, CUDA events, "
+         "best of %d\", \"sms\": %d, \"clock_khz_attr\": %d, \"fp4_tflops\": %.1f, "
+         "\"fp4_tflops_distinct_ab\": %.1f, \"int8_tops\": %.1f, \"int8_tops_distinct_ab\": %.1f, "
+         "\"err\": \"%s\"}\n",
+         reps, sms, clk, f4s, f4d, i8s, i8d, cudaGetErrorString(e));
+  return e == cudaSuccess ? 0 : 1;
+}
