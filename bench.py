@@ -817,7 +817,7 @@ def main():
     if not args.no_e2e:
         tx_bytes = P_band + P_band / 8
         kernels["transform"] = {
-            "bound": "hbm", "kernel": "k_pack_vec (binarize + bit-pack one raster)",
+            "bound": "hbm", "kernel": "k_pack_flat (binarize + bit-pack one raster)",
             "achieved": round(tx_bytes / kern_pack / 1e6, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(tx_bytes / kern_pack / 1e6 / hbm, 4), "kernel_ms": round(kern_pack, 4),
             "bytes_per_launch": int(tx_bytes), "bytes_def": "P raw read + P/8 packed write",

@@ -174,7 +174,9 @@ int fs_ensemble_sync(fs_ensemble *ens);
 /* Choose the Gram engine used by FS_GRAM_AUTO (process-wide; default FS_GRAM_TC_F4). */
 int fs_set_gram_engine(int engine);
 /* Choose the transform kernel: 0 = TMA bulk-staged, 1 = direct vector loads,
- * 2 = 8 coalesced 16-B loads in flight per thread (4 KB per warp). */
+ * 2 = 8 coalesced 16-B loads in flight per thread (4 KB per warp, persistent grid),
+ * 3 = 2 + next block's loads in flight and an in-kernel tail, 4 (default) = one 4 KB
+ * block per warp over a raster-sized grid, 16-B packed stores, in-kernel tail. */
 int fs_set_pack_engine(int engine);
 
 /* ---- native interactive-recompute loop (service.py:110-175 without the interpreter) ----
@@ -184,13 +186,31 @@ int fs_set_pack_engine(int engine);
  * [bins | Gram], Jaccard matrix and scores — while the workers run each finished frame's
  * complete-linkage merge (tau, id_rank as in fs_cluster_complete_linkage).  The last
  * frame's products go to the (optional) host outputs; *device_ms = device time of the
- * whole run (CUDA events on the ensemble's compute stream).  Single device.          */
+ * whole run (CUDA events on the ensemble's compute stream).  One device per pipeline;
+ * with an fs_comm attached (below) each rank runs its own band's pipeline and the
+ * partials are summed inside the loop.                                                 */
 typedef struct fs_pipeline fs_pipeline;
 int fs_pipeline_create(fs_ensemble *ens, const uint32_t *slots, uint32_t k, int engine, double tau,
                        const uint32_t *id_rank, uint32_t depth, fs_pipeline **out);
 int fs_pipeline_run(fs_pipeline *p, uint32_t n_frames, int64_t *bins, int64_t *gram, double *sim,
                     double *scores, int32_t *labels, double *device_ms);
 int fs_pipeline_destroy(fs_pipeline *p);
+
+/* ---- multi-GPU exchange (north_star: "partial Gram matrices are summed with NCCL
+ * allreduce"; replaces the reference's single-process analytics.py:174-181 loop when the
+ * raster is split into row bands, one band per rank) -------------------------------------
+ * An fs_comm is an NCCL communicator on the calling thread's device; libnccl is loaded at
+ * run time (the copy torch already mapped, else libnccl.so.2).  Rank 0 creates the id,
+ * the caller ships its 128 bytes to every rank (torch.distributed in dist.py), and every
+ * rank calls fs_comm_create with it.  fs_pipeline_set_comm makes every frame of
+ * fs_pipeline_run sum the [bins | Gram] partials of all ranks (int64, exact) on the
+ * ensemble stream before the Jaccard / outlier kernels; NULL detaches.                 */
+typedef struct fs_comm fs_comm;
+int fs_comm_unique_id(uint8_t *out /* 128 bytes */);
+int fs_comm_create(const uint8_t *id /* 128 bytes */, int nranks, int rank, fs_comm **out);
+int fs_comm_allreduce_i64(fs_comm *c, int64_t *buf, uint64_t n, void *stream);
+int fs_comm_destroy(fs_comm *c);
+int fs_pipeline_set_comm(fs_pipeline *p, fs_comm *c);
 
 /* ---- pinned host memory (for zero-staging uploads and fast read-back) ---- */
 int fs_host_alloc(uint64_t bytes, void **out);

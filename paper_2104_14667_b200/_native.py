@@ -104,6 +104,11 @@ _SIGNATURES = {
                            C.POINTER(_vp)],
     "fs_pipeline_run": [_vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, C.POINTER(C.c_double)],
     "fs_pipeline_destroy": [_vp],
+    "fs_pipeline_set_comm": [_vp, _vp],
+    "fs_comm_unique_id": [_vp],
+    "fs_comm_create": [_vp, C.c_int, C.c_int, C.POINTER(_vp)],
+    "fs_comm_allreduce_i64": [_vp, _vp, C.c_uint64, _vp],
+    "fs_comm_destroy": [_vp],
 }
 
 EXPORTED_SYMBOLS = ("fs_last_error",) + tuple(_SIGNATURES)

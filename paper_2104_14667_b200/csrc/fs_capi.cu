@@ -274,7 +274,7 @@ int fs_set_gram_engine(int engine) {
   return FS_OK;
 }
 int fs_set_pack_engine(int engine) {
-  if (engine < 0 || engine > 3) return set_err(FS_EINVAL, "unknown pack engine");
+  if (engine < 0 || engine > 4) return set_err(FS_EINVAL, "unknown pack engine");
   set_pack_engine(engine);
   return FS_OK;
 }
@@ -1594,7 +1594,7 @@ int fs_time_transform(uint32_t width, uint32_t height, int reps, int engine, dou
                       double *us_min) {
   if (!us_mean || !us_min) return set_err(FS_EINVAL, "null out");
   if (width == 0 || height == 0 || reps < 1) return set_err(FS_EINVAL, "bad sweep cell");
-  if (engine < -1 || engine > 3) return set_err(FS_EINVAL, "unknown pack engine");
+  if (engine < -1 || engine > 4) return set_err(FS_EINVAL, "unknown pack engine");
   ThreadCtx *c;
   int rc = get_ctx(&c);
   if (rc) return rc;

@@ -56,7 +56,7 @@ __device__ __forceinline__ uint32_t nz_bits16(uint4 v) {
 constexpr int kPackThreads = 256;
 constexpr int kPackChunk = 8192;  // bytes (= pixels) per stage, 256 output words
 constexpr int kPackStages = 4;
-static int g_pack_engine = 2;  // k_pack_vec: measured fastest (profiles/r1x)
+static int g_pack_engine = 4;  // k_pack_flat: measured fastest (profiles/round2)
 void set_pack_engine(int e) { g_pack_engine = e; }
 int get_pack_engine() { return g_pack_engine; }
 
@@ -193,6 +193,48 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Flat variant (the default): one 4 KB block per warp, no loop — the grid is the raster
+// (ceil(blocks / 8) CTAs), so the whole read is in flight as soon as the CTAs land, which
+// measured best against a cold L2 (profiles/round2/pack_probe.json: "flat").  The warp's
+// 128 packed words go through 512 B of shared memory so each lane writes one 16-B vector
+// (4 x 128-B tile rows per warp instead of 64-B half-rows); trailing CTAs pack the partial
+// last block and the zero padding up to wpm in the same launch.
+__global__ void __launch_bounds__(256)
+    k_pack_flat(const uint8_t *__restrict__ src, uint64_t pixels, uint64_t wpm,
+                uint32_t *__restrict__ dst, uint64_t slot, uint64_t cap) {
+  __shared__ __align__(16) uint32_t stage[8][kPackBlk / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t nblk = pixels / kPackBlk;
+  const uint64_t body_ctas = (nblk + 7) / 8;
+  if (blockIdx.x < body_ctas) {
+    const uint64_t b = (uint64_t)blockIdx.x * 8 + wib;
+    if (b >= nblk) return;
+    const uint8_t *base = src + b * kPackBlk + lane * 16;
+    uint4 v[kPackVec];
+#pragma unroll
+    for (int i = 0; i < kPackVec; ++i) v[i] = ptx::ld_nc_v4(base + i * 512);
+#pragma unroll
+    for (int i = 0; i < kPackVec; ++i) {
+      const uint32_t h = nz_bits16(v[i]);
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
+      if ((lane & 1) == 0) stage[wib][i * 16 + (lane >> 1)] = h | (other << 16);
+    }
+    __syncwarp();
+    const uint4 q = *reinterpret_cast<const uint4 *>(&stage[wib][4 * lane]);
+    // words 4 lane .. 4 lane + 3 of the block: one tile row (pk_off is contiguous within a
+    // 32-word tile and 4 lane never crosses one)
+    *reinterpret_cast<uint4 *>(dst + pk_off(slot, b * (kPackBlk / 32) + 4 * lane, cap)) = q;
+    return;
+  }
+  // partial last block + zero padding: words [nblk * 128, wpm), one word per thread
+  const uint64_t w = nblk * (kPackBlk / 32) + (blockIdx.x - body_ctas) * 256ull + threadIdx.x;
+  if (w >= wpm) return;
+  uint32_t word = 0;
+  const uint64_t p0 = w * 32;
+  for (int q = 0; q < 32 && p0 + q < pixels; ++q) word |= (uint32_t)(src[p0 + q] != 0) << q;
+  dst[pk_off(slot, w, cap)] = word;
+}
+
 // Words [w0, wpm): scalar tail + zero padding.
 __global__ void k_pack_tail(const uint8_t *__restrict__ src, uint64_t pixels, uint64_t w0,
                             uint64_t wpm, uint32_t *__restrict__ dst, uint64_t slot,
@@ -226,6 +268,12 @@ cudaError_t launch_pack(const uint8_t *src, uint64_t pixels, uint32_t *dst, uint
       k_pack_bulk<<<(unsigned)grid, kPackThreads, smem, s>>>(src, nchunks, dst, slot, cap);
       done_words = nchunks * (kPackChunk / 32);
     }
+  } else if (engine == 4) {
+    const uint64_t nblk = pixels / kPackBlk;
+    const uint64_t tail = wpm - nblk * (kPackBlk / 32);
+    const uint64_t grid = (nblk + 7) / 8 + (tail + 255) / 256;
+    if (grid > 0) k_pack_flat<<<(unsigned)grid, 256, 0, s>>>(src, pixels, wpm, dst, slot, cap);
+    return cudaGetLastError();
   } else if (engine == 3) {
     const uint64_t nblk = pixels / kPackBlk;
     uint64_t grid = (std::max<uint64_t>(nblk, 1) * 32 + 255) / 256;

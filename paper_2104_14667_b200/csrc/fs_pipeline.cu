@@ -6,6 +6,14 @@
 // frame f+1's device work — fused recompute, Jaccard + outlier kernels, D2H of the
 // partials — is queued while host worker threads run frame f's complete-linkage merge,
 // with a ring of `depth` frame buffers (device outputs + pinned host slots + events).
+//
+// Multi-GPU: an fs_comm (an NCCL communicator, libnccl loaded at run time — the copy
+// torch already mapped when there is one) attached with fs_pipeline_set_comm sums the
+// row bands' int64 [bins | Gram] partials with one ncclAllReduce on the ensemble stream
+// inside every frame (north_star: partial Gram matrices summed with NCCL allreduce), so
+// each rank's loop runs frame after frame without returning to Python.
+#include <dlfcn.h>
+
 #include <condition_variable>
 #include <cstring>
 #include <deque>
@@ -18,6 +26,63 @@
 
 #include "../../include/floodstream.h"
 #include "fs_internal.h"
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time (no link-time dependency; ABI of nccl.h 2.x)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct NcclUniqueId {
+  char internal[128];
+};
+using ncclComm_t = void *;
+constexpr int kNcclInt64 = 4, kNcclSum = 0;  // ncclInt64, ncclSum
+
+struct NcclApi {
+  int (*get_unique_id)(NcclUniqueId *) = nullptr;
+  int (*comm_init_rank)(ncclComm_t *, int, NcclUniqueId, int) = nullptr;
+  int (*comm_destroy)(ncclComm_t) = nullptr;
+  int (*all_reduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char *(*error_string)(int) = nullptr;
+  std::string error;
+  bool ok = false;
+};
+
+const NcclApi &nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // torch's copy, if mapped
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      const char *e = dlerror();
+      a.error = std::string("libnccl not found: ") + (e ? e : "dlopen failed");
+      return a;
+    }
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_reduce;
+    if (!a.ok) a.error = "libnccl lacks ncclGetUniqueId/ncclCommInitRank/ncclAllReduce";
+    return a;
+  }();
+  return api;
+}
+
+std::string nccl_msg(const char *what, int r) {
+  const NcclApi &a = nccl();
+  return std::string(what) + ": " + (a.error_string ? a.error_string(r) : "nccl error") +
+         " (" + std::to_string(r) + ")";
+}
+
+}  // namespace
+
+struct fs_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+};
 
 namespace {
 
@@ -42,6 +107,7 @@ struct fs_pipeline {
   double tau = 0.8;
   uint64_t pixels = 0;
   int device = 0;
+  fs_comm *comm = nullptr;  // optional: sum [bins | Gram] over the row bands every frame
   cudaStream_t side = nullptr;
   std::vector<Frame> frames;
   std::vector<std::thread> workers;
@@ -195,6 +261,17 @@ int fs_pipeline_run(fs_pipeline *p, uint32_t n_frames, int64_t *bins, int64_t *g
       f.busy = false;
       break;
     }
+    if (p->comm != nullptr) {
+      // the exact int64 sum of every band's [bins | Gram] (one bucket per frame)
+      const int r = nccl().all_reduce(f.d_part, f.d_part, nb + (size_t)k * k, kNcclInt64, kNcclSum,
+                                      p->comm->comm, (cudaStream_t)sk);
+      if (r != 0) {
+        rc = fail(FS_ECUDA, nccl_msg("ncclAllReduce", r));
+        std::lock_guard<std::mutex> lk(p->mu);
+        f.busy = false;
+        break;
+      }
+    }
     // Jaccard + outliers and the small D2H on the side stream, behind the recompute
     cudaEventRecord(ready, (cudaStream_t)sk);
     cudaStreamWaitEvent(p->side, ready, 0);
@@ -249,6 +326,58 @@ int fs_pipeline_run(fs_pipeline *p, uint32_t n_frames, int64_t *bins, int64_t *g
   }
   cudaSetDevice(prev);
   return rc;
+}
+
+int fs_pipeline_set_comm(fs_pipeline *p, fs_comm *c) {
+  if (!p) return fail(FS_EINVAL, "null pipeline");
+  if (c != nullptr && c->device != p->device)
+    return fail(FS_EINVAL, "communicator and pipeline are on different devices");
+  p->comm = c;
+  return FS_OK;
+}
+
+int fs_comm_unique_id(uint8_t *out) {
+  if (!out) return fail(FS_EINVAL, "null out");
+  const NcclApi &a = nccl();
+  if (!a.ok) return fail(FS_ECUDA, a.error);
+  NcclUniqueId id;
+  const int r = a.get_unique_id(&id);
+  if (r != 0) return fail(FS_ECUDA, nccl_msg("ncclGetUniqueId", r));
+  std::memcpy(out, id.internal, sizeof(id.internal));
+  return FS_OK;
+}
+
+int fs_comm_create(const uint8_t *id, int nranks, int rank, fs_comm **out) {
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(FS_EINVAL, "bad communicator arguments");
+  const NcclApi &a = nccl();
+  if (!a.ok) return fail(FS_ECUDA, a.error);
+  auto c = std::make_unique<fs_comm>();
+  c->nranks = nranks;
+  c->rank = rank;
+  if (cudaGetDevice(&c->device) != cudaSuccess) return fail(FS_ENODEV, "no CUDA device");
+  NcclUniqueId uid;
+  std::memcpy(uid.internal, id, sizeof(uid.internal));
+  const int r = a.comm_init_rank(&c->comm, nranks, uid, rank);
+  if (r != 0) return fail(FS_ECUDA, nccl_msg("ncclCommInitRank", r));
+  *out = c.release();
+  return FS_OK;
+}
+
+int fs_comm_allreduce_i64(fs_comm *c, int64_t *buf, uint64_t n, void *stream) {
+  if (!c || (!buf && n)) return fail(FS_EINVAL, "bad allreduce arguments");
+  if (n == 0) return FS_OK;
+  const int r = nccl().all_reduce(buf, buf, (size_t)n, kNcclInt64, kNcclSum, c->comm,
+                                  (cudaStream_t)stream);
+  return r == 0 ? FS_OK : fail(FS_ECUDA, nccl_msg("ncclAllReduce", r));
+}
+
+int fs_comm_destroy(fs_comm *c) {
+  if (!c) return FS_OK;
+  int r = 0;
+  if (c->comm) r = nccl().comm_destroy(c->comm);
+  delete c;
+  return r == 0 ? FS_OK : fail(FS_ECUDA, nccl_msg("ncclCommDestroy", r));
 }
 
 int fs_pipeline_destroy(fs_pipeline *p) {

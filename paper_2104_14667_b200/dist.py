@@ -69,6 +69,51 @@ def gather_rows(local, height: int, group=None, dst: int = 0):
     return torch.cat([parts[r][: band(height, r, world)[1]] for r in range(world)], dim=0)
 
 
+class NativeComm:
+    """An NCCL communicator inside libfloodstream (fs_comm_*) for this rank's device, so
+    the native frame loop (fs_pipeline_run) can sum the bands' [bins | Gram] partials
+    itself.  Rank 0 draws the NCCL unique id; it reaches the other ranks through the
+    torch.distributed group (any backend) — torch stays plumbing, the per-frame exchange
+    runs in C++ on the ensemble stream."""
+
+    def __init__(self, group=None, device: int | None = None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            N.call("fs_comm_unique_id", uid)
+        if self.world > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0)
+                                       if group is not None else 0, group=group)
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        dev = torch.cuda.current_device() if device is None else int(device)
+        N.set_device(dev)
+        h = C.c_void_p()
+        N.call("fs_comm_create", uid, self.world, self.rank, C.byref(h))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            N.load().fs_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class ShardedEnsemble:
     """This rank's row band of a bit-packed ensemble plus the exchange step.
 
@@ -103,7 +148,20 @@ class ShardedEnsemble:
         if getattr(self, "_pool", None) is not None:
             self._pool.shutdown(wait=True)
             self._pool = None
+        if getattr(self, "_comm", None) is not None:
+            self._comm.close()
+            self._comm = None
         self.ens.close()
+
+    def pipeline(self, slots=None, *, tau: float = 0.8, engine: str = "auto", depth: int = 3,
+                 ids=None):
+        """The native frame loop (fs_pipeline_*) on this rank's band with the per-frame
+        all-reduce of the [bins | Gram] partials inside it (fs_comm, NCCL): every rank
+        ends each frame with the GLOBAL histogram, Gram, Jaccard, outliers and clusters."""
+        if getattr(self, "_comm", None) is None:
+            self._comm = NativeComm(self.group, device=self.device.index)
+        return self.ens.pipeline(slots, tau=tau, engine=engine, depth=depth, ids=ids,
+                                 comm=self._comm)
 
     def _make_buffers(self, k: int, n_inputs: int, maps: bool):
         import torch

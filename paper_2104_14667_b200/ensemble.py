@@ -273,11 +273,12 @@ class DeviceEnsemble:
         return c, b, r, g, bool(fused.value)
 
     def pipeline(self, slots=None, *, tau: float = 0.8, engine: str = "auto", depth: int = 3,
-                 ids=None) -> "NativePipeline":
+                 ids=None, comm=None) -> "NativePipeline":
         """Native frame loop over ``slots`` (fs_pipeline_*): recompute, device Jaccard /
-        outliers, D2H and host linkage overlapped in C++ (single device)."""
+        outliers, D2H and host linkage overlapped in C++.  ``comm`` (dist.NativeComm):
+        this ensemble is one rank's row band and every frame sums the bands' partials."""
         return NativePipeline(self, self._slots(slots), tau=tau, engine=engine, depth=depth,
-                              ids=ids)
+                              ids=ids, comm=comm)
 
     def recompute(self, slots=None, *, tau: float = 0.8, engine: str = "auto",
                   overlap: bool = True, pairwise: bool = True) -> Snapshot:
@@ -309,7 +310,7 @@ class NativePipeline:
     (include/floodstream.h, fs_pipeline_*).  ``run(n)`` returns the last frame's products."""
 
     def __init__(self, ens: DeviceEnsemble, slots: np.ndarray, *, tau: float, engine: str,
-                 depth: int, ids=None):
+                 depth: int, ids=None, comm=None):
         self.ens = ens
         self.slots = np.ascontiguousarray(slots, dtype=np.uint32)
         self.k = int(self.slots.size)
@@ -325,6 +326,9 @@ class NativePipeline:
                _GRAM_ENGINES[engine], self.tau, self.rank.ctypes.data_as(N._u32p), int(depth),
                C.byref(h))
         self._h = h
+        self.comm = comm
+        if comm is not None:
+            N.call("fs_pipeline_set_comm", h, comm.handle)
 
     def run(self, n_frames: int) -> dict:
         k = self.k

@@ -74,6 +74,23 @@ def main():
         assert np.array_equal(r["rgba"], x["rgba"][row0:row0 + rows])
         assert np.array_equal(r["gram"], x["gram"])
         checks["sharded_frames"] = len(frames)
+        # the native frame loop with the exchange inside it (fs_comm = NCCL).  NCCL refuses
+        # two ranks of one communicator on the same GPU ("Duplicate GPU"); these boxes have
+        # one GPU, so that refusal is recorded instead of a result.
+        try:
+            with sh.pipeline(range(k), tau=0.6, ids=ids) as pipe:
+                r = pipe.run(3)
+            x = want[order[-1]]
+            assert r["bins"].tolist() == x["bins"].tolist()
+            assert np.array_equal(r["gram"], x["gram"])
+            assert r["similarity"].tobytes() == x["sim"].tobytes()
+            assert r["outliers"] == x["out"]
+            assert r["clusters"] == x["cl"]
+            checks["native_pipeline_nccl"] = "ok"
+        except N.NativeError as e:
+            if "duplicate" not in str(e).lower() and "invalid usage" not in str(e).lower():
+                raise
+            checks["native_pipeline_nccl"] = "nccl refused two ranks on one GPU: " + str(e)[:200]
     finally:
         sh.close()
 

@@ -278,3 +278,20 @@ def test_clustering_duplicate_ids_list_order(seed):
     ids = [str(v) for v in rng.integers(0, max(2, n // 3), n)]
     tau = float(rng.choice([0.2, 0.4, 0.6, 0.8]))
     assert cluster_from_similarity(s, ids, tau) == O.cluster(s, ids, tau)
+
+
+def test_comm_unique_id_without_gpu_and_create_needs_a_device():
+    """fs_comm_unique_id only asks libnccl for a bootstrap id (works on CPU); creating a
+    communicator needs a CUDA device and fails loudly without one."""
+    import ctypes as C
+
+    from paper_2104_14667_b200 import _native as N
+
+    uid = (C.c_uint8 * 128)()
+    N.call("fs_comm_unique_id", uid)
+    assert any(bytes(uid))
+    h = C.c_void_p()
+    with pytest.raises((RuntimeError, ValueError)):
+        N.call("fs_comm_create", uid, 1, 0, C.byref(h))
+    with pytest.raises(ValueError):
+        N.call("fs_comm_create", uid, 2, 5, C.byref(h))

@@ -200,8 +200,9 @@ def test_gram_large_pixels(engine):
 
 # ---- transform, synth ------------------------------------------------------------------
 
-@pytest.mark.parametrize("pixels", [1, 31, 8191, 8192, 8193, 3 * 8192 + 17, 1 << 20, 612 * 499])
-@pytest.mark.parametrize("engine", [0, 1, 2])
+@pytest.mark.parametrize("pixels", [1, 31, 4095, 4096, 4097, 8191, 8192, 8193, 3 * 8192 + 17,
+                                    9 * 4096 + 4095, 1 << 20, 612 * 499])
+@pytest.mark.parametrize("engine", [0, 1, 2, 3, 4])
 def test_pack_engines(pixels, engine):
     rng = np.random.default_rng(pixels)
     cells = [rng.integers(0, 3, pixels).astype(np.uint8).reshape(1, pixels) for _ in range(3)]
@@ -212,7 +213,7 @@ def test_pack_engines(pixels, engine):
             c, b, r = ens.overlap([0, 1, 2])
             g = ens.gram([0, 1, 2], engine="popc")
     finally:
-        N.call("fs_set_pack_engine", 2)
+        N.call("fs_set_pack_engine", 4)
     want = O.accumulate(cells, pixels, 1)
     assert np.array_equal(c, want)
     assert np.array_equal(g, O.gram(cells))

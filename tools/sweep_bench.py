@@ -33,7 +33,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--quick", action="store_true", help="8x8 grids (smoke)")
     ap.add_argument("--engine", type=int, default=-1,
-                    help="transform kernel: -1 default, 0 TMA bulk, 1 direct, 2 vector")
+                    help="transform kernel: -1 default (4), 0 TMA bulk, 1 direct, 2 vector, 3 pipelined, 4 flat")
     args = ap.parse_args()
 
     from paper_2104_14667_b200 import _native as N
@@ -52,7 +52,8 @@ def main():
     doc = {"config": "c5: raster dimension sweep 512-16384 (non-square, non-pow2), iid p=0.5",
            "kernel": {-1: "library default", 0: "k_pack_bulk (TMA bulk-staged)",
                       1: "k_pack_direct", 2: "k_pack_vec (8 x 16-B loads in flight)",
-                      3: "k_pack_pipe (next block's loads in flight, in-kernel tail)"}[args.engine]
+                      3: "k_pack_pipe (next block's loads in flight, in-kernel tail)",
+                      4: "k_pack_flat (one 4 KB block per warp, raster-sized grid, in-kernel tail)"}[args.engine]
                      + " binarize + bit-pack",
            "rate_def": "w*h / t_us / 1000 GB/s of uint8 raster (fs/bench.py:337-338)",
            "roofline": {"bound": "hbm", "bytes_per_px": 1.125, "peak_gbs": hbm,
