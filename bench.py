@@ -805,8 +805,8 @@ def main():
                 "fused": bool(fused), "achieved": round(gram_ops / rc_ms / 1e9, 1),
                 "peak": t_peak, "unit": "TFLOP/s",
                 "frac": round(gram_ops / rc_ms / 1e9 / t_peak, 4),
-                "traffic": traffic.get("k_gram_tc_fused") if one_panel else None,
-                "ncu": traffic.get("k_gram_tc_fused_ncu") if one_panel else None,
+                "traffic": traffic.get("k_recompute_f4") if one_panel and k > 128 else None,
+                "ncu": traffic.get("k_recompute_f4_ncu") if one_panel and k > 128 else None,
                 "kernel_ms": round(rc_ms, 4), "ops_per_launch": gram_ops, "ops_def": ops_def,
                 "peak_note": t_kind,
                 "hbm_achieved_gbs": round(ov_bytes / rc_ms / 1e6, 1),
@@ -821,7 +821,7 @@ def main():
             "achieved": round(tx_bytes / kern_pack / 1e6, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(tx_bytes / kern_pack / 1e6 / hbm, 4), "kernel_ms": round(kern_pack, 4),
             "bytes_per_launch": int(tx_bytes), "bytes_def": "P raw read + P/8 packed write",
-            "launches_per_step": k, "traffic": traffic.get("k_pack_vec_c2_raster")
+            "launches_per_step": k, "traffic": traffic.get("k_pack_flat_c2_raster")
             if (P_band == 8192 * 8192) else None}
 
     # ---- the same frames through the native C++ loop (single device, informational) ----

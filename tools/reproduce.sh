@@ -6,9 +6,9 @@
 #   evidence  the headline bench lines + the ncu launch list and the full capture of
 #             the dominant kernel (what a kernel change needs re-measured)
 #   tests     pytest -m gpu, smoke, the reference's own suite (three bindings)
-#   parts     part isolation of the fused recompute: rebuilds with FS_PROBE_* macros
-#             that drop one part each (timings of probe builds are NOT results); the
-#             shipped build is restored at the end
+#   parts     part isolation of the fused recompute: probe builds (tools/probe_builds.py)
+#             with FS_RC_* macros that drop one part each (timings of probe builds are
+#             NOT results); the shipped library is not touched
 #   sanitize  compute-sanitizer memcheck / racecheck / synccheck over every kernel family
 set -euo pipefail
 MODE=${1:-all}
@@ -33,21 +33,25 @@ evidence() {
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file "$O/launches_c2.csv" \
       python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu                > /dev/null
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gram_tc -s 2 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_recompute_f4 -s 2 -c 1 \
       -o "$O/c2_recompute_fused" python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pack_flat -s 8 -c 1 \
+      -o "$O/c2_pack_flat" python bench.py --steps 1 --warmup 3 --no-cpu > /dev/null
 }
 
 parts() {
-  local cases=16:8192:8192,128:8192:8192,256:8192:8192 i=0
-  for d in "" "-DFS_PROBE_NO_MMA" "-DFS_PROBE_NO_MMA -DFS_PROBE_NO_COUNT" \
-           "-DFS_PROBE_NO_MMA -DFS_PROBE_NO_EXPAND" "-DFS_PROBE_NO_MMA -DFS_PROBE_NO_EMIT" \
-           "-DFS_PROBE_NO_COUNT" "-DFS_PROBE_NO_MMA -DFS_PROBE_NO_COUNT -DFS_PROBE_NO_EXPAND"; do
-    FS_NVCC_EXTRA="$d" python -m paper_2104_14667_b200.build --force > /dev/null
-    echo "# $d" > "$O/v$i.jsonl"
-    python tools/k_sweep.py --fused-only --cases $cases >> "$O/v$i.jsonl" 2>&1
-    i=$((i + 1))
+  local cases=256:8192:8192,129:8192:8192
+  python tools/probe_builds.py nomma="-DFS_RC_NO_MMA" nocount="-DFS_RC_NO_COUNT" \
+      noexp="-DFS_RC_NO_EXPAND" noemit="-DFS_RC_NO_EMIT" noload="-DFS_RC_NO_LOAD" \
+      nopf="-DFS_RC_L2PF=0" batch1="-DFS_RC_BATCH=1" > /dev/null
+  for v in base nomma nocount noexp noemit noload nopf batch1; do
+    echo "# $v" >> "$O/parts.jsonl"
+    if [ "$v" = base ]; then
+      python tools/k_sweep.py --fused-only --cases $cases >> "$O/parts.jsonl" 2>&1
+    else
+      FS_LIB_PROBE="probes/$v.so" python tools/k_sweep.py --fused-only --cases $cases >> "$O/parts.jsonl" 2>&1
+    fi
   done
-  python -m paper_2104_14667_b200.build --force > /dev/null
 }
 
 sanitize() {
