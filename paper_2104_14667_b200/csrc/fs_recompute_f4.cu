@@ -8,39 +8,57 @@
 //
 // Data path per 1024-px unit (one pixel tile of every mask = 256 x 128 B, contiguous in
 // the tile-interleaved layout, fs_common.cuh):
-//   * 8 expander warps load the unit straight from global memory into REGISTERS with
-//     fully coalesced 16-B loads (warp instruction j covers 4 consecutive mask rows =
-//     512 contiguous bytes); lane l holds rows 4j + l/8 (j = 0..7) of its warp's 32
-//     rows, 16-B chunk c = l % 8 (pixels 128c .. 128c+127).  The next unit's loads are
-//     in flight while this one is processed (two register buffers): no TMA ring, no raw
-//     copy in shared memory at all.
+//   * Two groups of 8 expander warps take alternate units (FS_RC_GROUPS = 2; group g
+//     does units u = g mod 2), so a warp has two units of MMA time for one unit of its
+//     serial load / count / expand chain.  A warp loads its 32 rows of the unit straight
+//     from global memory into REGISTERS with fully coalesced 16-B loads (warp
+//     instruction j covers 4 consecutive mask rows = 512 contiguous bytes); lane l holds
+//     rows 4j + l/8 (j = 0..7), 16-B chunk c = l % 8 (pixels 128c .. 128c+127).  One lane
+//     per group bulk-prefetches the unit 4 ahead into L2 (cp.async.bulk.prefetch.L2), so
+//     the register loads, issued as soon as the previous unit is expanded, hit L2.  No
+//     TMA ring and no raw copy in shared memory.
 //   * Counting from those registers: per lane a carry-save tree over its 8 rows, then
 //     two shuffle rounds over the 4 lanes holding the same chunk give each lane the
 //     bit-sliced count (6 planes) of one 32-px word over the warp's 32 rows; the 8 warps'
-//     partial planes (6 KB per unit) go to shared memory and 4 combiner warps add them
-//     (9 planes, exact), transpose to per-pixel counts and emit histogram / counts /
-//     RGBA (fs_bitslice.cuh emit_tile).
+//     partial planes (6 KB per unit) go to a per-group partial ring in shared memory and
+//     3 combiner warps add them (9 planes, exact), transpose to per-pixel counts and emit
+//     histogram / counts / RGBA (fs_bitslice.cuh emit_tile).
 //   * Expansion from the same registers: operand stage s of the unit = word s of every
 //     chunk (any pixel permutation shared by all masks leaves a Gram unchanged), so each
 //     lane writes 16 B of e2m1 0/1 operand per row per stage into the SWIZZLE_128B
-//     K-major ring; one thread issues rows 0-127 x N=256 and rows 128-255 x N=128
-//     kind::mxf4 MMAs per 64-px K step (3/4 of the 256 x 256 square; the reduce mirrors).
-// Shared-memory traffic per 256-px stage: UMMA operand fetch + 32 KB expander stores +
-// ~3 KB partial counts + the emit staging — the raw tiles never pass through it.
+//     K-major ring (5 x 32 KB); one thread issues rows 0-127 x N=256 and rows 128-255 x
+//     N=128 kind::mxf4 MMAs per 64-px K step (3/4 of the 256 x 256 square; the reduce
+//     mirrors).
+// Measured (profiles/round2/kernel_search): the tensor core's operand fetch and the
+// expanders' st.shared stream do not compete (768 -> 778 cycles per stage with 32 KB of
+// stores beside the MMAs); what sets the time is the MMA pipe (90 % active under ncu) and
+// the handoff of each stage between the expander warps and the MMA thread.
 #include "fs_bitslice.cuh"
 #include "fs_tcgen05.cuh"
 
 namespace fs {
 namespace rc {
 
-constexpr int kExpWarps = 8;                  // expander / epilogue warps
-constexpr int kCntWarps = 4;                  // combiner + emit warps
+// Expander groups: 1 = eight expander warps take every unit (double-buffered registers);
+// 2 = two groups of eight take alternate units (single-buffered), so each warp has two
+// units of MMA time for one unit of its serial work (20 warps, 96 registers).
+#ifndef FS_RC_GROUPS
+#define FS_RC_GROUPS 2
+#endif
+constexpr int kGroups = FS_RC_GROUPS;
+static_assert(kGroups == 1 || kGroups == 2, "one or two expander groups");
+constexpr int kExpWarps = 8 * kGroups;        // expander / epilogue warps (8 per group)
+constexpr int kCntWarps = kGroups == 1 ? 4 : 3;  // combiner + emit warps
 constexpr int kWarps = 1 + kExpWarps + kCntWarps;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kCntWarp0 = 1 + kExpWarps;
-constexpr int kPartDepth = 4;                 // partial-count ring (multiple of kCntWarps)
+// partial-count ring: kCntWarps slots per group; combiner c owns slot c of every group's
+// ring and takes the units u with (u / kGroups) % kCntWarps == c, in order — one producer
+// group and one consumer per slot, so the parity waits cannot alias
+constexpr int kPartSlots = kCntWarps;
+constexpr int kPartDepth = kGroups * kPartSlots;
 constexpr int kPlanes = 6;                    // bit planes of a 32-row partial count
-constexpr int kPartWords = kExpWarps * kPlanes * 32;  // per unit
+constexpr int kPartWords = 8 * kPlanes * 32;  // per unit (eight warps of one group)
 constexpr int kStageBytes = 256 * 128;        // 256 rows x 128 B (256 px of e2m1)
 constexpr int kFuseBins = 288;
 constexpr int kTbBytes = kCntWarps * 32 * kTileTb * 4;
@@ -50,7 +68,7 @@ constexpr int kStages = (kSmemMax - 1024 - 512 - kExtraBytes) / kStageBytes;
 constexpr int kSmemBytes = kStages * kStageBytes + kExtraBytes + 1024 + 512;
 static_assert(kStages >= 3, "operand ring too shallow");
 #ifndef FS_RC_BATCH
-#define FS_RC_BATCH 2
+#define FS_RC_BATCH 1
 #endif
 #ifndef FS_RC_COUNT_MID
 #define FS_RC_COUNT_MID 0
@@ -68,7 +86,10 @@ static_assert(kStages >= 3, "operand ring too shallow");
 constexpr int kBatch = FS_RC_BATCH;             // operand stages per proxy fence
 constexpr bool kCountMid = FS_RC_COUNT_MID != 0;  // count between the two stage halves
 static_assert(4 % kBatch == 0 && kBatch < kStages, "batch must divide a unit's 4 stages");
-static_assert(kPartDepth % kCntWarps == 0, "combiner warp u % 4 must own partial slot u % depth");
+__host__ __device__ constexpr int part_slot(int u) {
+  return (u % kGroups) * kPartSlots + (u / kGroups) % kPartSlots;
+}
+__host__ __device__ constexpr int part_use(int u) { return (u / kGroups) / kPartSlots; }
 
 // bulk L2 prefetch of one unit (k rows x 128 B, contiguous)
 __device__ __forceinline__ void l2_prefetch(const void *p, uint32_t bytes) {
@@ -160,13 +181,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // expander registers: rows 4j + lane/8 of this warp's 32 rows, chunk lane % 8
   const int ew = warp - 1;
+  const int grp = ew / 8, gw = ew % 8;  // expander group, warp within the group
   const uint32_t chunk = (uint32_t)lane & 7u;
   uint4 ra[8], rb[8];
   auto load_unit = [&](int u, uint4 (&r)[8]) {
     const uint64_t gu = u0 + (uint64_t)u;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const uint32_t row = (uint32_t)(32 * ew + 4 * j) + ((uint32_t)lane >> 3);
+      const uint32_t row = (uint32_t)(32 * gw + 4 * j) + ((uint32_t)lane >> 3);
 #ifndef FS_RC_NO_LOAD  // timing experiment only: no HBM traffic, constant data
       if (row < a.k)
         r[j] = ptx::ld_nc_v4(a.src + ((gu * a.cap + a.row0 + row) * 32u + 4u * chunk));
@@ -180,18 +202,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
   const bool is_exp = warp >= 1 && warp <= kExpWarps;
-  if (is_exp) {  // first two units in flight before the setup below
-    if (nunits > 0) load_unit(0, ra);
-    if (nunits > 1) load_unit(1, rb);
+  if (is_exp) {  // first unit(s) in flight before the setup below
+    if (grp < nunits) load_unit(grp, ra);
+    if (kGroups == 1 && nunits > 1) load_unit(1, rb);
   }
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], kExpWarps);
+      ptx::mbar_init(&full[s], 8);  // the eight warps of the unit's group
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kPartDepth; ++s) {
-      ptx::mbar_init(&part_full[s], kExpWarps);
+      ptx::mbar_init(&part_full[s], 8);
       ptx::mbar_init(&part_empty[s], 1);
     }
     ptx::mbar_init(tmem_full, 1);
@@ -293,9 +315,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // this lane now holds word 4c + 2 b3 + b4 of the unit (c = lane % 8)
       const uint32_t wi = 4u * chunk + 2u * (uint32_t)b3 + (uint32_t)b4;
-      const int ps = u % kPartDepth;
-      if (u >= kPartDepth) ptx::mbar_wait(&part_empty[ps], (uint32_t)(((u / kPartDepth) - 1) & 1));
-      uint32_t *dst = part + ps * kPartWords + ew * kPlanes * 32;
+      const int ps = part_slot(u), pu = part_use(u);
+      if (pu > 0) ptx::mbar_wait(&part_empty[ps], (uint32_t)((pu - 1) & 1));
+      uint32_t *dst = part + ps * kPartWords + gw * kPlanes * 32;
 #pragma unroll
       for (int p = 0; p < kPlanes; ++p) dst[p * 32 + wi] = R6[p];
       __syncwarp();
@@ -316,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sbase = op_base + (uint32_t)((u * 4 + s) % kStages) * kStageBytes;
 #pragma unroll
         for (int jr = 0; jr < 8; ++jr) {
-          const uint32_t row = (uint32_t)(32 * ew + 4 * jr) + sw_lo;
+          const uint32_t row = (uint32_t)(32 * gw + 4 * jr) + sw_lo;
           const uint32_t swz = (sw_lo + 4u * (uint32_t)(jr & 1)) & 7u;
           const uint32_t w = s == 0 ? r[jr].x : s == 1 ? r[jr].y : s == 2 ? r[jr].z : r[jr].w;
 #ifndef FS_RC_NO_EXPAND  // timing experiment only
@@ -335,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     auto process = [&](int u, uint4 (&r)[8]) {
 #if FS_RC_L2PF > 0
-      if (ew == 0 && lane == 0 && u + FS_RC_L2PF < nunits)
+      if (gw == 0 && lane == 0 && u + FS_RC_L2PF < nunits)
         l2_prefetch(a.src + ((u0 + (uint64_t)(u + FS_RC_L2PF)) * a.cap + a.row0) * 32u, a.k * 128u);
 #endif
       if (!kCountMid) count_unit(u, r);
@@ -345,24 +367,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (kCountMid && s0 + kBatch == 2) count_unit(u, r);
       }
     };
-    for (int u = 0; u < nunits; u += 2) {
-      process(u, ra);
-      if (u + 2 < nunits) load_unit(u + 2, ra);
-      if (u + 1 < nunits) {
-        process(u + 1, rb);
-        if (u + 3 < nunits) load_unit(u + 3, rb);
+    if (kGroups == 1) {
+      for (int u = 0; u < nunits; u += 2) {
+        process(u, ra);
+        if (u + 2 < nunits) load_unit(u + 2, ra);
+        if (u + 1 < nunits) {
+          process(u + 1, rb);
+          if (u + 3 < nunits) load_unit(u + 3, rb);
+        }
+      }
+    } else {
+      // this group's units; the next one is requested as soon as the registers are free
+      // (the other group's unit and the operand ring cover its latency)
+      for (int u = grp; u < nunits; u += kGroups) {
+        process(u, ra);
+        if (u + kGroups < nunits) load_unit(u + kGroups, ra);
       }
     }
     // ===== epilogue: TMEM -> registers -> int32 partial tile =====
     const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp
-    const int cg = (warp - 1) / 4;            // two warps per quarter split the columns
+    const int cg = gw / 4;                    // two warps per quarter split the columns
     int32_t *out = a.partial + (uint64_t)blockIdx.x * 256 * 256;
-    if (nst > 0) {
+    if (grp == 0 && nst > 0) {
       ptx::mbar_wait(tmem_full, 0);
       tc::fence_after();
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < 2 && grp == 0; ++h) {  // group 0 drains the accumulators
       const uint32_t row = h * 128 + q * 32 + lane;
       const int c_begin = h == 1 ? 128 : 0;
       for (int c0 = c_begin + 32 * cg; c0 < 256; c0 += 64) {
@@ -386,12 +417,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ===== combiners: 8 partial counts -> exact per-pixel counts -> emit =====
     const int cw = warp - kCntWarp0;
-    for (int u = cw; u < nunits; u += kCntWarps) {
+    for (int u0c = cw * kGroups, u = u0c; u < nunits;
+         u = (u % kGroups == kGroups - 1) ? u + 1 + (kCntWarps - 1) * kGroups : u + 1) {
 #ifdef FS_RC_NO_COUNT  // timing experiment only
       break;
 #endif
-      const int ps = u % kPartDepth;
-      ptx::mbar_wait(&part_full[ps], (uint32_t)((u / kPartDepth) & 1));
+      const int ps = part_slot(u);
+      ptx::mbar_wait(&part_full[ps], (uint32_t)(part_use(u) & 1));
       const uint32_t *src = part + ps * kPartWords + lane;
       uint32_t n[8][kPlanes];
 #pragma unroll

@@ -299,14 +299,19 @@ class ShardedEnsemble:
         k = int(sl.size)
         ids = list(ids) if ids is not None else [f"s{i:04d}" for i in sl.tolist()]
         depth = max(2, int(depth))
+        # one ring of frame buffers per (k, maps, depth), kept across calls: pinned
+        # host slots cost milliseconds per MiB to allocate, so switching between map and
+        # map-less frames must not reallocate them (at most two rings are kept)
         key = (k, maps_to_host, depth)
-        if self._bufs.get("key") != key:
-            self._bufs = {"key": key,
-                          "b": [self._make_buffers(k, k, maps_to_host) for _ in range(depth)],
-                          "free": [threading.Event() for _ in range(depth)]}
-            for e in self._bufs["free"]:
+        if key not in self._bufs:
+            if len(self._bufs) >= 2:
+                self._bufs.pop(next(iter(self._bufs)))
+            ring = {"b": [self._make_buffers(k, k, maps_to_host) for _ in range(depth)],
+                    "free": [threading.Event() for _ in range(depth)]}
+            for e in ring["free"]:
                 e.set()
-        bufs, free = self._bufs["b"], self._bufs["free"]
+            self._bufs[key] = ring
+        bufs, free = self._bufs[key]["b"], self._bufs[key]["free"]
         pool = self._executor(depth)
         # "all": every rank runs the host analytics; "root": rank 0 only; "none": skip
         analytics = analytics_ranks == "all" or (analytics_ranks == "root" and self.rank == 0)

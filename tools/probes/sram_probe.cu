@@ -126,6 +126,38 @@ __global__ void __launch_bounds__(288, 1)
     }
     commit(&done_bar);
     mbar_wait(&done_bar, 0);
+  } else if (threadIdx.x >= 32 && (mode & 8)) {
+    // split: warps 1-4 store sts_per_stage x 512 B per stage with st.shared.v4, warps 5-8
+    // stream sts_per_stage / 4 x 512 B per stage of global memory (the expanders' raw
+    // units: a quarter of the expanded bytes), 8 x 16-B loads in flight per thread
+    const int w = (threadIdx.x >> 5) - 1, lane = threadIdx.x & 31;
+    if (w < 4) {
+      const int per_warp = (stages * sts_per_stage) / 4;
+      uint32_t x = threadIdx.x * 2654435761u;
+      for (int i = 0; i < per_warp; ++i) {
+        const uint32_t off = (uint32_t)(((w * 977 + i) * 512) & (kStsRegion - 1)) + lane * 16;
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sts_base + off), "r"(x),
+                     "r"(x + 1), "r"(x + 2), "r"(x + 3));
+        x += 0x9E3779B9u;
+      }
+    } else {
+      const int per_warp = (stages * sts_per_stage / 4) / 4;
+      uint32_t acc = 0;
+      const uint4 *p = gsrc + ((size_t)blockIdx.x * 4 + (w - 4)) * 32 + lane;
+      for (int i = 0; i < per_warp; i += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const size_t off = ((size_t)(i + j) * 148 * 4 * 32) & ((1ull << 26) - 1);
+          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v[j].x), "=r"(v[j].y), "=r"(v[j].z), "=r"(v[j].w)
+                       : "l"(p + off));
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc ^= v[j].x ^ v[j].w;
+      }
+      if (acc == 0x12345678u) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sts_base), "r"(acc));
+    }
   } else if (threadIdx.x >= 32 && (mode & 4)) {
     // 8 warps stream global memory (16-B loads, 8 in flight per thread), like the expanders
     const int w = (threadIdx.x >> 5) - 1, lane = threadIdx.x & 31;
@@ -184,7 +216,8 @@ int main() {
   const Case cases[] = {{0, 1, 0, "mma zeros"},        {0, 1, 1, "mma data"},
                         {64, 2, 0, "sts 32KB"},         {64, 3, 1, "mma data + sts 32KB"},
                         {64, 4, 0, "ldg 32KB"},         {64, 5, 1, "mma data + ldg 32KB"},
-                        {128, 4, 0, "ldg 64KB"},        {128, 5, 1, "mma data + ldg 64KB"}};
+                        {128, 4, 0, "ldg 64KB"},        {128, 5, 1, "mma data + ldg 64KB"},
+                        {64, 8, 0, "sts 32KB + ldg 8KB"}, {64, 9, 1, "mma data + sts 32KB + ldg 8KB"}};
   for (const Case &c : cases) {
     unsigned long long cyc = 0;
     k_probe<<<148, 288, kSmem>>>(stages / 8, c.sts, c.mode, d, g, c.fill);  // warm-up
