@@ -46,6 +46,12 @@ namespace rc {
 #define FS_RC_GROUPS 2
 #endif
 constexpr int kGroups = FS_RC_GROUPS;
+// histogram by warp-aggregated atomics (__match_any_sync per pixel position) instead of
+// per-lane run-length atomics
+#ifndef FS_RC_HIST_MATCH
+#define FS_RC_HIST_MATCH 1
+#endif
+constexpr bool kHistMatch = FS_RC_HIST_MATCH != 0;
 static_assert(kGroups == 1 || kGroups == 2, "one or two expander groups");
 constexpr int kExpWarps = 8 * kGroups;        // expander / epilogue warps (8 per group)
 constexpr int kCntWarps = kGroups == 1 ? 4 : 3;  // combiner + emit warps
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (cnt32[lane & 31] == 0xFFFFFFFFu) ov.counts[0] = 0;  // keep the count live
       continue;
 #endif
-      emit_tile(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
+      emit_tile<kHistMatch>(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
                 ov.bins != nullptr, sh_lut, lut_sh);
     }
   }

@@ -42,7 +42,9 @@ def main():
     assert np.array_equal(out, want)
     print("primitives ok", flush=True)
 
-    for (w, h, k) in [(130, 33, 20), (96, 20, 256), (64, 40, 300)]:
+    # (1024, 1024, 144): the fused k <= 256 recompute with ~7 units per CTA, so both
+    # expander groups, the operand ring and the partial rings wrap several times
+    for (w, h, k) in [(130, 33, 20), (96, 20, 256), (1024, 1024, 144), (64, 40, 300)]:
         cells = [synth_cells(w, h, i, members=5, eps=0.05) for i in range(k)]
         with DeviceEnsemble(w, h, k) as ens:
             ens.stream(cells, variant="2b-final", with_kernel=True)
