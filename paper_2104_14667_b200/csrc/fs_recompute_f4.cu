@@ -49,9 +49,16 @@ constexpr int kGroups = FS_RC_GROUPS;
 // histogram by warp-aggregated atomics (__match_any_sync per pixel position) instead of
 // per-lane run-length atomics
 #ifndef FS_RC_HIST_MATCH
-#define FS_RC_HIST_MATCH 1
+#define FS_RC_HIST_MATCH 0
 #endif
 constexpr bool kHistMatch = FS_RC_HIST_MATCH != 0;
+// every producing thread arrives on the stage / partial barriers itself (the arrive is the
+// release of that thread's own stores; 1) or one lane per warp after __syncwarp (0)
+#ifndef FS_RC_THREAD_ARRIVE
+#define FS_RC_THREAD_ARRIVE 1
+#endif
+constexpr bool kThreadArrive = FS_RC_THREAD_ARRIVE != 0;
+constexpr uint32_t kArrivePerWarp = kThreadArrive ? 32u : 1u;
 static_assert(kGroups == 1 || kGroups == 2, "one or two expander groups");
 constexpr int kExpWarps = 8 * kGroups;        // expander / epilogue warps (8 per group)
 constexpr int kCntWarps = kGroups == 1 ? 4 : 3;  // combiner + emit warps
@@ -215,12 +222,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], 8);  // the eight warps of the unit's group
+      ptx::mbar_init(&full[s], 8 * kArrivePerWarp);  // the eight warps of the unit's group
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kPartDepth; ++s) {
-      ptx::mbar_init(&part_full[s], 8);
-      ptx::mbar_init(&part_empty[s], 1);
+      ptx::mbar_init(&part_full[s], 8 * kArrivePerWarp);
+      ptx::mbar_init(&part_empty[s], kArrivePerWarp);
     }
     ptx::mbar_init(tmem_full, 1);
     ptx::fence_mbar_init();
@@ -326,8 +333,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t *dst = part + ps * kPartWords + gw * kPlanes * 32;
 #pragma unroll
       for (int p = 0; p < kPlanes; ++p) dst[p * 32 + wi] = R6[p];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&part_full[ps]);
+      if (kThreadArrive) {
+        ptx::mbar_arrive(&part_full[ps]);
+      } else {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&part_full[ps]);
+      }
 #endif
     };
     // --- operand stages s0 .. s0 + kBatch - 1 of unit u: word s of every chunk of every
@@ -355,8 +366,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       ptx::fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
+      if (!kThreadArrive) __syncwarp();
+      if (kThreadArrive || lane == 0) {
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) ptx::mbar_arrive(&full[(u * 4 + s0 + b) % kStages]);
       }
@@ -436,8 +447,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int w = 0; w < 8; ++w)
 #pragma unroll
         for (int p = 0; p < kPlanes; ++p) n[w][p] = src[(w * kPlanes + p) * 32];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&part_empty[ps]);
+      if (kThreadArrive) {
+        ptx::mbar_arrive(&part_empty[ps]);
+      } else {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&part_empty[ps]);
+      }
       uint32_t s7[4][7], s8[2][8], s9[9];
 #pragma unroll
       for (int i = 0; i < 4; ++i) add_planes<6>(n[2 * i], n[2 * i + 1], s7[i]);
