@@ -62,7 +62,8 @@ class OpNode:
 
 @dataclass
 class ScheduleGraph:
-    """Ordered node list; the order is also the per-channel enqueue order."""
+    """The DAG of one pipeline run as a node list; listing order doubles as the order in
+    which each channel (copy / compute) receives its work."""
 
     nodes: list[OpNode] = field(default_factory=list)
     pairs: int = 1

@@ -141,7 +141,8 @@ def closed_form_times(c: Sequence[int], m: Sequence[int], p: Sequence[int]) -> t
 
 
 def efficiency(c: Sequence[int], t_total: int) -> float:
-    """Fraction of the run spent doing irreducible bus copies."""
+    """Copy-bound share of a run: the sum of the per-item copy times over the measured
+    total (the paper's efficiency)."""
     if t_total <= 0:
         raise StreamError("total time must be positive")
     return sum(c) / t_total

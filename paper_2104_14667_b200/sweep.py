@@ -34,7 +34,8 @@ class BenchError(ValueError):
 
 @dataclass(frozen=True)
 class SweepSpec:
-    """Square sweep over image dimensions: start..max in fixed steps."""
+    """The dimension grid of a transform sweep: widths and heights from ``start`` up to
+    ``max`` every ``step`` pixels (fs/bench.py:55-76 schema)."""
 
     start: int
     step: int
@@ -60,8 +61,8 @@ class SweepSpec:
 
 @dataclass
 class RateMap:
-    """Transform rates (GB/s of raster) over a dimension sweep: ``rates[r, c]`` is the
-    rate at width ``start + c*step`` and height ``start + r*step``."""
+    """Measured transform throughput on the sweep grid, in GB/s of uint8 raster; row r is
+    height ``start + r*step`` and column c width ``start + c*step``."""
 
     spec: SweepSpec
     rates: np.ndarray = field(repr=False)
@@ -82,7 +83,8 @@ class RateMap:
                        rates=np.asarray(doc["rates"], dtype=np.float64))
 
     def to_csv(self) -> str:
-        """Calibration-CSV rows ``width,height,rate_gbps``."""
+        """One ``width,height,rate_gbps`` line per grid cell (the reference's calibration CSV
+        layout)."""
         buf = io.StringIO()
         wr = csv.writer(buf)
         wr.writerow(["width", "height", "rate_gbps"])
@@ -225,7 +227,8 @@ VARIANTS = ("1b-initial", "2b-initial", "1b-final", "2b-final")
 
 
 def resolve_dims(entry) -> tuple[str, int, int]:
-    """'4k', 'WxH' or (w, h) -> (label, w, h) (bench.py:167-181)."""
+    """Normalise an image-size argument — a named size ('2k', '4k', '8k'), a 'WxH'
+    string or a (w, h) pair — to (label, width, height) (fs/bench.py:167-181)."""
     if isinstance(entry, str):
         if entry in DIMS:
             return (entry,) + DIMS[entry]
