@@ -6,7 +6,8 @@
 // one commit.  The kernel is timed with CUDA events (best of `reps`), so the figure is
 // what the chip sustains at its own clock, not a cycles x nominal-clock product.
 // "same" reuses one 128-row operand as A and B (no operand-fetch limit); "distinct" reads
-// A and a separate 256-row B (the fetch-bound case).  Prints one JSON object; the
+// A and a separate 256-row B (the fetch-bound case).  The sustained figures run
+// back-to-back launches for 4 s (zeros, and 0/1 data that draws real switching power).  Prints one JSON object; the
 // fp4_tflops / int8_tops keys feed profiles/tensor_peaks.json.
 //
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tc_peak tc_peak.cu
@@ -52,8 +53,17 @@ __global__ void __launch_bounds__(128, 1) k_peak(int iters, int distinct) {
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tslot;
   const uint32_t base = (smem_u32(sm) + 1023u) & ~1023u;
-  for (int i = threadIdx.x; i < (48 * 1024) / 16; i += blockDim.x)
-    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(base + 16 * i), "r"(0));
+  // operands: zeros, or (distinct >= 2) e2m1 0 / 1.0 nibbles (int8 0 / 2) from a hash —
+  // switching data draws the power real masks do
+  for (int i = threadIdx.x; i < (48 * 1024) / 16; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ 0x5bd1e995u;
+    h ^= h >> 15;
+    h *= 0x2c1b3c6du;
+    h ^= h >> 12;
+    const uint32_t v = distinct >= 2 ? (h & 0x22222222u) : 0u;
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(base + 16 * i), "r"(v),
+                 "r"(v ^ 0x20202020u), "r"(v ^ 0x02020202u), "r"(v ^ 0x22002200u));
+  }
   if (threadIdx.x == 0) mbar_init(&done_bar, 1);
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -85,7 +95,7 @@ __global__ void __launch_bounds__(128, 1) k_peak(int iters, int distinct) {
   if (threadIdx.x == 0) {
     const uint32_t id = FP4 ? idesc_mxf4(128, 256) : idesc_i8(128, 256);
     const uint32_t sfa = tmem + 448u, sfb = tmem + 464u;
-    const uint32_t a_base = base, b_base = distinct ? base + 16 * 1024 : base;
+    const uint32_t a_base = base, b_base = (distinct & 1) ? base + 16 * 1024 : base;
     for (int j = 0; j < iters; ++j) {
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
@@ -141,6 +151,41 @@ static double run(int sms, int iters, int distinct, int reps) {
   return ops / (best * 1e-3) / 1e12;
 }
 
+// Sustained: back-to-back launches for `seconds`, rate over the last half (the chip has
+// settled at its power-capped clock by then).
+template <bool FP4>
+static double run_sustained(int sms, int iters, double seconds, bool data) {
+  const int smem = 64 * 1024;
+  cudaFuncSetAttribute(k_peak<FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float elapsed = 0.f;
+  int launches = 0;
+  cudaEventRecord(a);
+  while (elapsed < seconds * 1e3f) {  // run until `seconds` have passed
+    for (int r = 0; r < 8; ++r) k_peak<FP4><<<sms, 128, smem>>>(iters, data ? 2 : 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&elapsed, a, b);
+  }
+  cudaEventRecord(a);  // second half: measured
+  const float t0 = elapsed;
+  elapsed = 0.f;
+  while (elapsed < t0 * 0.5f) {
+    for (int r = 0; r < 8; ++r) k_peak<FP4><<<sms, 128, smem>>>(iters, data ? 2 : 0);
+    launches += 8;
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&elapsed, a, b);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  const double k_per = FP4 ? 64.0 : 32.0;
+  const double ops = 2.0 * 128 * 256 * k_per * 4.0 * iters * sms * (double)launches;
+  return ops / (elapsed * 1e-3) / 1e12;
+}
+
 int main() {
   int sms = 0, dev = 0, clk = 0;
   cudaGetDevice(&dev);
@@ -149,11 +194,13 @@ int main() {
   const int iters = 1 << 16, reps = 5;
   const double f4s = run<true>(sms, iters, 0, reps), f4d = run<true>(sms, iters, 1, reps);
   const double i8s = run<false>(sms, iters, 0, reps), i8d = run<false>(sms, iters, 1, reps);
+  const double f4sus = run_sustained<true>(sms, 1 << 14, 4.0, false);
+  const double f4sus_data = run_sustained<true>(sms, 1 << 14, 4.0, true);
   const cudaError_t e = cudaDeviceSynchronize();
   printf("{\"probe\": \"tcgen05.mma M=128 N=256 back to back, one CTA per SM, CUDA events, "
          "best of %d\", \"sms\": %d, \"clock_khz_attr\": %d, \"fp4_tflops\": %.1f, "
          "\"fp4_tflops_distinct_ab\": %.1f, \"int8_tops\": %.1f, \"int8_tops_distinct_ab\": %.1f, "
-         "\"err\": \"%s\"}\n",
-         reps, sms, clk, f4s, f4d, i8s, i8d, cudaGetErrorString(e));
+         "\"fp4_tflops_sustained\": %.1f, \"fp4_tflops_sustained_data\": %.1f, \"err\": \"%s\"}\n",
+         reps, sms, clk, f4s, f4d, i8s, i8d, f4sus, f4sus_data, cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : 1;
 }
