@@ -488,6 +488,16 @@ constexpr int kPairDepth = 2;      // raw units in flight per CTA
 constexpr int kPairRawUnit = 2 * 128 * 128;  // A half + B half, 1024 px (128 B) per row
 constexpr int kPairStageBytes = 2 * 128 * 128;  // A + B operand halves, 256 px per row
 constexpr int kPairStages = 5;
+// raw units prefetched into L2 ahead of the TMA loads (0 = off)
+#ifndef FS_PAIR_L2PF
+#define FS_PAIR_L2PF 0
+#endif
+// operand stages per proxy fence (1 or 2; a raw unit holds 4 stages)
+#ifndef FS_PAIR_BATCH
+#define FS_PAIR_BATCH 2
+#endif
+constexpr int kPairBatch = FS_PAIR_BATCH;
+static_assert(kPairBatch == 1 || kPairBatch == 2, "1 or 2 stages per fence");
 constexpr int kPairSmemBytes = kPairDepth * kPairRawUnit + kPairStages * kPairStageBytes + 1024 + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -632,6 +642,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     if (lane == 0) {
       for (int u = 0; u < nunits; ++u) {
         const int ru = u % kPairDepth;
+#if FS_PAIR_L2PF > 0
+        if (u == 0)
+          for (int q = 1; q <= FS_PAIR_L2PF && q < nunits; ++q) {
+            ptx::tma_prefetch_3d(&tm, 0, (int)(I * 256 + rank * 128), (int)(u0 + (uint64_t)q));
+            ptx::tma_prefetch_3d(&tm, 0, (int)(J * 256 + rank * 128), (int)(u0 + (uint64_t)q));
+          }
+        else if (u + FS_PAIR_L2PF < nunits) {
+          const int cp = (int)(u0 + (uint64_t)(u + FS_PAIR_L2PF));
+          ptx::tma_prefetch_3d(&tm, 0, (int)(I * 256 + rank * 128), cp);
+          ptx::tma_prefetch_3d(&tm, 0, (int)(J * 256 + rank * 128), cp);
+        }
+#endif
         if (u >= kPairDepth) ptx::mbar_wait(&raw_empty[ru], (uint32_t)(((u / kPairDepth) - 1) & 1));
         const int c2 = (int)(u0 + (uint64_t)u);
         ptx::mbar_arrive_expect_tx(&raw_full[ru], kPairRawUnit);
@@ -659,27 +681,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     };
     uint4 v0, v1;
     bool have = false;
-    for (int j = 0; j < nst; ++j) {
-      const int u = j / kSub, sub = j % kSub;
-      const int ru = u % kPairDepth;
-      const int s = j % kPairStages;
-      if (!have) load(j, v0, v1);
-      if (j >= kPairStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / kPairStages) - 1) & 1));
-      const uint32_t obase = op_base + s * kPairStageBytes + reg * 128 * 128;
-      expand_row_f4(obase, rr, 0u, v0);
-      expand_row_f4(obase, rr, 4u, v1);
-      uint4 n0, n1;
-      have = j + 1 < nst && (j + 1) % kSub != 0;
-      if (have) load(j + 1, n0, n1);
-      ptx::fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_cluster(&full[s], 0);
-        if (sub == kSub - 1) ptx::mbar_arrive(&raw_empty[ru]);
+    if (kPairBatch == 1) {
+      for (int j = 0; j < nst; ++j) {
+        const int u = j / kSub, sub = j % kSub;
+        const int ru = u % kPairDepth;
+        const int s = j % kPairStages;
+        if (!have) load(j, v0, v1);
+        if (j >= kPairStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / kPairStages) - 1) & 1));
+        const uint32_t obase = op_base + s * kPairStageBytes + reg * 128 * 128;
+        expand_row_f4(obase, rr, 0u, v0);
+        expand_row_f4(obase, rr, 4u, v1);
+        uint4 n0, n1;
+        have = j + 1 < nst && (j + 1) % kSub != 0;
+        if (have) load(j + 1, n0, n1);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_cluster(&full[s], 0);
+          if (sub == kSub - 1) ptx::mbar_arrive(&raw_empty[ru]);
+        }
+        if (have) {
+          v0 = n0;
+          v1 = n1;
+        }
       }
-      if (have) {
-        v0 = n0;
-        v1 = n1;
+    } else {
+      // two stages per proxy fence: stages j, j + 1 (same raw unit) expanded back to back
+      for (int j = 0; j < nst; j += 2) {
+        const int u = j / kSub, sub = j % kSub;
+        const int ru = u % kPairDepth;
+        const int s0 = j % kPairStages, s1 = (j + 1) % kPairStages;
+        uint4 w0, w1;
+        load(j, v0, v1);
+        load(j + 1, w0, w1);
+        if (j >= kPairStages) ptx::mbar_wait(&empty[s0], (uint32_t)(((j / kPairStages) - 1) & 1));
+        if (j + 1 >= kPairStages)
+          ptx::mbar_wait(&empty[s1], (uint32_t)((((j + 1) / kPairStages) - 1) & 1));
+        const uint32_t ob0 = op_base + s0 * kPairStageBytes + reg * 128 * 128;
+        const uint32_t ob1 = op_base + s1 * kPairStageBytes + reg * 128 * 128;
+        expand_row_f4(ob0, rr, 0u, v0);
+        expand_row_f4(ob0, rr, 4u, v1);
+        expand_row_f4(ob1, rr, 0u, w0);
+        expand_row_f4(ob1, rr, 4u, w1);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_cluster(&full[s0], 0);
+          mbar_arrive_cluster(&full[s1], 0);
+          if (sub + 1 == kSub - 1) ptx::mbar_arrive(&raw_empty[ru]);
+        }
       }
     }
     // ===== epilogue: this CTA's 128 rows x 256 columns of D =====
@@ -971,6 +1021,9 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
     else if (fuse_now)
       e = fp4 ? launch_one<256, true, true, true, tc::kFuseDepth256>(tm_diag, p, part_diag, *fuse, s)
               : launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s);
+    else if (fuse_multi && fused_kernel_version() >= 2)
+      e = launch_recompute_f4(src, src_cap, row0, k, p.units_diag, p.kc_diag, p.upc_diag,
+                              part_diag, ovp, s, p.ndiag);
     else if (fuse_multi)
       e = launch_one<256, true, true, true, tc::kFuseDepth256>(tm_diag, p, part_diag, ovp, s);
     else

@@ -117,9 +117,13 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
 // The fused recompute of one 129..256-mask FP4 panel (fs_recompute_f4.cu): Gram partial
 // tiles (one 256 x 256 int32 tile per CTA chunk of upc units) + the overlap products of
 // `ov` (counts / histogram / RGBA, bins zeroed by the caller) from one read of the masks.
+// npanels > 1: the diagonal 256-mask tiles of a larger ensemble, panel-major CTAs
+// (blockIdx = panel * kchunks + chunk); with ov.partial16 set each panel's counts go to
+// its uint16 slab (ov.part_pitch apart) for launch_combine_partials.
 cudaError_t launch_recompute_f4(const uint32_t *src, uint64_t cap, uint64_t row0, uint32_t k,
                                 uint64_t total_units, uint32_t kchunks, uint64_t upc,
-                                int32_t *partial, const OverlapArgs &ov, cudaStream_t s);
+                                int32_t *partial, const OverlapArgs &ov, cudaStream_t s,
+                                uint32_t npanels = 1);
 // fuse != nullptr: when all k masks fit one panel (k <= 256) the diagonal CTAs also
 // run the overlap pass (counts / histogram / RGBA of `*fuse`, weights 1) and *fused is
 // set; bins must be zeroed by the caller.  Otherwise nothing of *fuse is written.

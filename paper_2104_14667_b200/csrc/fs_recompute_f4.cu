@@ -160,10 +160,11 @@ __device__ __forceinline__ void expand_word(uint32_t addr, uint32_t x) {
 struct Args {
   const uint32_t *src;   // packed masks (tile-interleaved)
   uint64_t cap;          // slots per tile row of `src`
-  uint64_t row0;         // first slot of the panel
-  uint32_t k;            // masks in the panel (<= 256)
+  uint64_t row0;         // first slot of panel 0
+  uint32_t k;            // masks in all panels (panel I holds masks 256 I .. 256 I + 255)
   uint64_t total_units;  // tiles of 1024 px
   uint64_t upc;          // units per CTA chunk
+  uint32_t kchunks;      // CTA chunks per panel: blockIdx.x = panel * kchunks + chunk
   int32_t *partial;      // one 256 x 256 int32 tile per CTA
 };
 
@@ -187,7 +188,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const uint64_t u0 = (uint64_t)blockIdx.x * a.upc;
+  // diagonal tile `panel` of a k > 256 ensemble (the Gram of masks 256 panel ..) or the
+  // single panel (panel 0); the off-diagonal tiles run on k_gram_pair_f4
+  const uint32_t panel = blockIdx.x / a.kchunks;
+  const uint64_t prow0 = a.row0 + 256ull * panel;            // first slot of this panel
+  const uint32_t pk = min(256u, a.k - 256u * panel);         // masks in this panel
+  const uint64_t u0 = (uint64_t)(blockIdx.x % a.kchunks) * a.upc;
   const uint64_t u1 = min(u0 + a.upc, a.total_units);
   const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
   const int nst = nunits * 4;
@@ -203,11 +209,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < 8; ++j) {
       const uint32_t row = (uint32_t)(32 * gw + 4 * j) + ((uint32_t)lane >> 3);
 #ifndef FS_RC_NO_LOAD  // timing experiment only: no HBM traffic, constant data
-      if (row < a.k)
-        r[j] = ptx::ld_nc_v4(a.src + ((gu * a.cap + a.row0 + row) * 32u + 4u * chunk));
+      if (row < pk)
+        r[j] = ptx::ld_nc_v4(a.src + ((gu * a.cap + prow0 + row) * 32u + 4u * chunk));
       else
 #else
-      if (row < a.k)
+      if (row < pk)
         r[j] = make_uint4((uint32_t)gu * 0x9E3779B9u ^ row, row * 7u, (uint32_t)gu, row ^ 5u);
       else
 #endif
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto process = [&](int u, uint4 (&r)[8]) {
 #if FS_RC_L2PF > 0
       if (gw == 0 && lane == 0 && u + FS_RC_L2PF < nunits)
-        l2_prefetch(a.src + ((u0 + (uint64_t)(u + FS_RC_L2PF)) * a.cap + a.row0) * 32u, a.k * 128u);
+        l2_prefetch(a.src + ((u0 + (uint64_t)(u + FS_RC_L2PF)) * a.cap + prow0) * 32u, pk * 128u);
 #endif
       if (!kCountMid) count_unit(u, r);
 #pragma unroll
@@ -472,8 +478,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (cnt32[lane & 31] == 0xFFFFFFFFu) ov.counts[0] = 0;  // keep the count live
       continue;
 #endif
-      emit_tile<kHistMatch>(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
-                ov.bins != nullptr, sh_lut, lut_sh);
+      if (ov.partial16 != nullptr)  // several panels: this panel's counts, summed later
+        emit_partial16(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb,
+                       ov.partial16 + (uint64_t)panel * ov.part_pitch);
+      else
+        emit_tile<kHistMatch>(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov,
+                              sh_hist, ov.bins != nullptr, sh_lut, lut_sh);
     }
   }
   __syncthreads();
@@ -495,13 +505,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 cudaError_t launch_recompute_f4(const uint32_t *src, uint64_t cap, uint64_t row0, uint32_t k,
                                 uint64_t total_units, uint32_t kchunks, uint64_t upc,
-                                int32_t *partial, const OverlapArgs &ov, cudaStream_t s) {
-  if (kchunks == 0) return cudaSuccess;
+                                int32_t *partial, const OverlapArgs &ov, cudaStream_t s,
+                                uint32_t npanels) {
+  if (kchunks == 0 || npanels == 0) return cudaSuccess;
   static SmemOptIn attr;
   if (cudaError_t e = smem_opt_in(attr, rc::k_recompute_f4, (size_t)rc::kSmemBytes); e != cudaSuccess)
     return e;
-  rc::Args a{src, cap, row0, k, total_units, upc, partial};
-  rc::k_recompute_f4<<<kchunks, rc::kThreads, rc::kSmemBytes, s>>>(a, ov);
+  rc::Args a{src, cap, row0, k, total_units, upc, kchunks, partial};
+  rc::k_recompute_f4<<<kchunks * npanels, rc::kThreads, rc::kSmemBytes, s>>>(a, ov);
   return cudaGetLastError();
 }
 
