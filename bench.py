@@ -4,8 +4,8 @@
 Workload (BASELINE.json configs[1], "c2"): 256 flood-like masks of 8192 x 8192 uint8
 (17.18 GB) in PINNED host memory.  One *step* = one full frame through the public API:
   H2D of every raster (2b-final dual-buffer DAG) overlapped with the binarize+pack
-  transform; ONE fused kernel for overlap counts + histogram + composite RGBA + the
-  exact pairwise-intersection Gram (tcgen05 kind::mxf4 + counter warps); Jaccard
+  transform; ONE fused kernel (k_recompute_f4) for overlap counts + histogram + composite
+  RGBA + the exact pairwise-intersection Gram (tcgen05 kind::mxf4); Jaccard
   matrix and outlier scores on the device; D2H of counts + RGBA + [bins | Gram] +
   Jaccard + scores; complete-linkage clusters (tau 0.8) on the host.
 
@@ -19,8 +19,10 @@ Workload (BASELINE.json configs[1], "c2"): 256 flood-like masks of 8192 x 8192 u
   against HBM; ``e2e.roofline`` is the step against measured pinned PCIe H2D.
 * ``--impl reference``: the reference's own CPU implementation — the unmodified
   reference package (baseline/_ref) run as shipped (single thread, numpy and cython
-  backends) and as an all-cores pixel-stripe harness around its unchanged primitives,
-  on the same workload; the all-cores number is the line's value.
+  backends, reported under ``as_shipped``) and on all host cores around its unchanged
+  primitives, where each step is a proportional sample of the frame (per-pixel ops over
+  all masks and pair_counts over ALL pairs on a window of rows): the all-cores number,
+  pixels / step time, is the line's value.
 
 Multi-GPU (torchrun, one rank per GPU): STRONG scaling by default — the fixed ensemble
 is cut into N row bands, rank r owns rows band(H, r, N) of every mask (one contiguous
