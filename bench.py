@@ -801,7 +801,7 @@ def main():
     rl_fused = {"bound": "tensor",
                 "kernel": (("k_recompute_f4 + k_gram_reduce" if k > 128 else
                             "k_gram_tc<128,...,FUSE> + k_gram_reduce") if npanels_k == 1 else
-                           "k_gram_tc<...,FUSE> (partial counts) + k_gram_pair_f4 + "
+                           "k_recompute_f4 diagonal tiles (partial counts) + k_gram_pair_f4 + "
                            "k_gram_reduce + k_combine_partials") if fused
                 else "k_overlap + k_gram_tc + k_gram_reduce",
                 "fused": bool(fused), "achieved": round(gram_ops / rc_ms / 1e9, 1),
