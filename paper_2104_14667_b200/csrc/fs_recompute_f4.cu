@@ -74,8 +74,14 @@ constexpr int kPlanes = 6;                    // bit planes of a 32-row partial 
 constexpr int kPartWords = 8 * kPlanes * 32;  // per unit (eight warps of one group)
 constexpr int kStageBytes = 256 * 128;        // 256 rows x 128 B (256 px of e2m1)
 constexpr int kFuseBins = 288;
+// one private SMEM histogram per combiner warp (1) or one shared by all of them (0)
+#ifndef FS_RC_PRIV_HIST
+#define FS_RC_PRIV_HIST 0
+#endif
+constexpr int kHistCopies = FS_RC_PRIV_HIST ? (FS_RC_GROUPS == 1 ? 4 : 3) : 1;  // = kCntWarps
 constexpr int kTbBytes = kCntWarps * 32 * kTileTb * 4;
-constexpr int kExtraBytes = kPartDepth * kPartWords * 4 + kTbBytes + 2 * kFuseBins * 4;
+constexpr int kExtraBytes =
+    kPartDepth * kPartWords * 4 + kTbBytes + (kHistCopies + 1) * kFuseBins * 4;
 constexpr int kSmemMax = 232448;
 constexpr int kStages = (kSmemMax - 1024 - 512 - kExtraBytes) / kStageBytes;
 constexpr int kSmemBytes = kStages * kStageBytes + kExtraBytes + 1024 + 512;
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *part = reinterpret_cast<uint32_t *>(smem + kStages * kStageBytes);
   uint32_t *cnt_tb = part + kPartDepth * kPartWords;
   uint32_t *sh_hist = cnt_tb + kCntWarps * 32 * kTileTb;
-  uint32_t *sh_lut = sh_hist + kFuseBins;
+  uint32_t *sh_lut = sh_hist + kHistCopies * kFuseBins;
   uint64_t *full = reinterpret_cast<uint64_t *>(sh_lut + kFuseBins);
   uint64_t *empty = full + kStages;
   uint64_t *part_full = empty + kStages;
@@ -241,7 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool lut_sh = ov.rgba != nullptr;
   if (warp >= kCntWarp0) {
     for (int i = tid - 32 * kCntWarp0; i < kFuseBins; i += 32 * kCntWarps) {
-      sh_hist[i] = 0;
+#pragma unroll
+      for (int c = 0; c < kHistCopies; ++c) sh_hist[c * kFuseBins + i] = 0;
       sh_lut[i] = lut_sh && (uint32_t)i < ov.nbins ? rgba_word(i, ov.n_inputs, ov.lut) : 0u;
     }
   }
@@ -483,13 +490,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                        ov.partial16 + (uint64_t)panel * ov.part_pitch);
       else
         emit_tile<kHistMatch>(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov,
-                              sh_hist, ov.bins != nullptr, sh_lut, lut_sh);
+                              sh_hist + (kHistCopies > 1 ? cw * kFuseBins : 0),
+                              ov.bins != nullptr, sh_lut, lut_sh);
     }
   }
   __syncthreads();
   if (warp >= kCntWarp0 && ov.bins != nullptr) {
-    for (uint32_t i = tid - 32 * kCntWarp0; i < ov.nbins; i += 32 * kCntWarps)
-      if (sh_hist[i]) atomicAdd(ov.bins + i, (unsigned long long)sh_hist[i]);
+    for (uint32_t i = tid - 32 * kCntWarp0; i < ov.nbins; i += 32 * kCntWarps) {
+      uint32_t h = 0;
+#pragma unroll
+      for (int c = 0; c < kHistCopies; ++c) h += sh_hist[c * kFuseBins + i];
+      if (h) atomicAdd(ov.bins + i, (unsigned long long)h);
+    }
     if (blockIdx.x == 0 && tid == 32 * kCntWarp0) {
       const uint64_t padpx = a.total_units * 1024 - ov.pixels;  // padding counted in bin 0
       if (padpx) atomicAdd(ov.bins, (unsigned long long)(0ull - padpx));
