@@ -958,8 +958,13 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
   uint64_t src_cap = capacity, row0 = 0;
   const int64_t first = contiguous_run(host_slots, k);
   cudaError_t e;
+  // the single-panel fused recompute reads scattered slots itself (no gather pass)
+  const bool rc_direct = fuse != nullptr && p.npanels == 1 && fp4 && p.panel == 256 &&
+                         fused_kernel_version() >= 2;
   if (first >= 0) {
     row0 = (uint64_t)first;
+  } else if (rc_direct) {
+    // src stays the ensemble; launch_recompute_f4 gets the slot list below
   } else {
     if (gather_ws == nullptr) return cudaErrorInvalidValue;
     uint64_t total = ntiles * k * 8;
@@ -1017,7 +1022,7 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
   } else {
     if (fuse_now && fp4 && fused_kernel_version() >= 2)
       e = launch_recompute_f4(src, src_cap, row0, k, p.units_diag, p.kc_diag, p.upc_diag,
-                              part_diag, *fuse, s);
+                              part_diag, *fuse, s, 1, first >= 0 ? nullptr : slots);
     else if (fuse_now)
       e = fp4 ? launch_one<256, true, true, true, tc::kFuseDepth256>(tm_diag, p, part_diag, *fuse, s)
               : launch_one<256, true, false, true>(tm_diag, p, part_diag, *fuse, s);

@@ -80,8 +80,9 @@ constexpr int kFuseBins = 288;
 #endif
 constexpr int kHistCopies = FS_RC_PRIV_HIST ? (FS_RC_GROUPS == 1 ? 4 : 3) : 1;  // = kCntWarps
 constexpr int kTbBytes = kCntWarps * 32 * kTileTb * 4;
-constexpr int kExtraBytes =
-    kPartDepth * kPartWords * 4 + kTbBytes + (kHistCopies + 1) * kFuseBins * 4;
+constexpr int kSlotWords = 256 + 2;  // slot of every panel row + the slot span [lo, hi]
+constexpr int kExtraBytes = kPartDepth * kPartWords * 4 + kTbBytes +
+                            (kHistCopies + 1) * kFuseBins * 4 + kSlotWords * 4;
 constexpr int kSmemMax = 232448;
 constexpr int kStages = (kSmemMax - 1024 - 512 - kExtraBytes) / kStageBytes;
 constexpr int kSmemBytes = kStages * kStageBytes + kExtraBytes + 1024 + 512;
@@ -168,6 +169,8 @@ struct Args {
   uint64_t cap;          // slots per tile row of `src`
   uint64_t row0;         // first slot of panel 0
   uint32_t k;            // masks in all panels (panel I holds masks 256 I .. 256 I + 255)
+  const uint32_t *slots; // device slot list (mask m lives in slot slots[m]) or null:
+                         // mask m in slot row0 + m (a contiguous run)
   uint64_t total_units;  // tiles of 1024 px
   uint64_t upc;          // units per CTA chunk
   uint32_t kchunks;      // CTA chunks per panel: blockIdx.x = panel * kchunks + chunk
@@ -185,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *cnt_tb = part + kPartDepth * kPartWords;
   uint32_t *sh_hist = cnt_tb + kCntWarps * 32 * kTileTb;
   uint32_t *sh_lut = sh_hist + kHistCopies * kFuseBins;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sh_lut + kFuseBins);
+  uint32_t *sh_slot = sh_lut + kFuseBins;  // ensemble slot of panel row r; [256], [257]: span
+  uint64_t *full = reinterpret_cast<uint64_t *>(sh_slot + kSlotWords);
   uint64_t *empty = full + kStages;
   uint64_t *part_full = empty + kStages;
   uint64_t *part_empty = part_full + kPartDepth;
@@ -215,8 +219,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < 8; ++j) {
       const uint32_t row = (uint32_t)(32 * gw + 4 * j) + ((uint32_t)lane >> 3);
 #ifndef FS_RC_NO_LOAD  // timing experiment only: no HBM traffic, constant data
-      if (row < pk)
-        r[j] = ptx::ld_nc_v4(a.src + ((gu * a.cap + prow0 + row) * 32u + 4u * chunk));
+      if (row < pk) {
+        const uint64_t slot = a.slots ? (uint64_t)sh_slot[row] : prow0 + row;
+        r[j] = ptx::ld_nc_v4(a.src + ((gu * a.cap + slot) * 32u + 4u * chunk));
+      }
       else
 #else
       if (row < pk)
@@ -227,10 +233,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
   const bool is_exp = warp >= 1 && warp <= kExpWarps;
-  if (is_exp) {  // first unit(s) in flight before the setup below
+  auto first_loads = [&] {
     if (grp < nunits) load_unit(grp, ra);
     if (kGroups == 1 && nunits > 1) load_unit(1, rb);
-  }
+  };
+  // a contiguous run: first unit(s) in flight before the setup below (a slot list is
+  // read into shared memory by the setup first)
+  if (is_exp && a.slots == nullptr) first_loads();
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -245,6 +254,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_mbar_init();
   }
   const bool lut_sh = ov.rgba != nullptr;
+  if (warp == kCntWarp0 && a.slots != nullptr) {  // this panel's slots and their span
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+    for (uint32_t i = (uint32_t)lane; i < 256u; i += 32u) {
+      const uint32_t sl = i < pk ? a.slots[256u * panel + i] : 0u;
+      sh_slot[i] = sl;
+      if (i < pk) {
+        lo = min(lo, sl);
+        hi = max(hi, sl);
+      }
+    }
+    lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+    hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+    if (lane == 0) {
+      sh_slot[256] = lo;
+      sh_slot[257] = hi;
+    }
+  }
   if (warp >= kCntWarp0) {
     for (int i = tid - 32 * kCntWarp0; i < kFuseBins; i += 32 * kCntWarps) {
 #pragma unroll
@@ -261,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  if (is_exp && a.slots != nullptr) first_loads();
   const uint32_t tmem = *tmem_slot;
   if (warp >= 1 && warp <= 4) {  // every UE8M0 block scale = 1.0
     const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
@@ -387,8 +414,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     auto process = [&](int u, uint4 (&r)[8]) {
 #if FS_RC_L2PF > 0
-      if (gw == 0 && lane == 0 && u + FS_RC_L2PF < nunits)
-        l2_prefetch(a.src + ((u0 + (uint64_t)(u + FS_RC_L2PF)) * a.cap + prow0) * 32u, pk * 128u);
+      if (gw == 0 && lane == 0 && u + FS_RC_L2PF < nunits) {
+        // the unit's rows: a contiguous run, or the span of the slot list when it is
+        // not much wider than the panel
+        const uint64_t lo = a.slots ? (uint64_t)sh_slot[256] : prow0;
+        const uint32_t n = a.slots ? sh_slot[257] - sh_slot[256] + 1u : pk;
+        if (n <= 2u * pk)
+          l2_prefetch(a.src + ((u0 + (uint64_t)(u + FS_RC_L2PF)) * a.cap + lo) * 32u, n * 128u);
+      }
 #endif
       if (!kCountMid) count_unit(u, r);
 #pragma unroll
@@ -518,12 +551,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 cudaError_t launch_recompute_f4(const uint32_t *src, uint64_t cap, uint64_t row0, uint32_t k,
                                 uint64_t total_units, uint32_t kchunks, uint64_t upc,
                                 int32_t *partial, const OverlapArgs &ov, cudaStream_t s,
-                                uint32_t npanels) {
+                                uint32_t npanels, const uint32_t *slots) {
   if (kchunks == 0 || npanels == 0) return cudaSuccess;
   static SmemOptIn attr;
   if (cudaError_t e = smem_opt_in(attr, rc::k_recompute_f4, (size_t)rc::kSmemBytes); e != cudaSuccess)
     return e;
-  rc::Args a{src, cap, row0, k, total_units, upc, kchunks, partial};
+  rc::Args a{src, cap, row0, k, slots, total_units, upc, kchunks, partial};
   rc::k_recompute_f4<<<kchunks * npanels, rc::kThreads, rc::kSmemBytes, s>>>(a, ov);
   return cudaGetLastError();
 }
