@@ -80,6 +80,11 @@ constexpr int kFuseBins = 288;
 #endif
 constexpr int kHistCopies = FS_RC_PRIV_HIST ? (FS_RC_GROUPS == 1 ? 4 : 3) : 1;  // = kCntWarps
 constexpr int kTbBytes = kCntWarps * 32 * kTileTb * 4;
+// emit counts / RGBA straight from each lane's 32 consecutive pixels (1) or through the
+// shared-memory transpose of emit_tile (0)
+#ifndef FS_RC_DIRECT_EMIT
+#define FS_RC_DIRECT_EMIT 0
+#endif
 constexpr int kSlotWords = 256 + 2;  // slot of every panel row + the slot span [lo, hi]
 constexpr int kExtraBytes = kPartDepth * kPartWords * 4 + kTbBytes +
                             (kHistCopies + 1) * kFuseBins * 4 + kSlotWords * 4;
@@ -164,6 +169,53 @@ __device__ __forceinline__ void expand_word(uint32_t addr, uint32_t x) {
                                     (x >> 1) & 0x22222222u, (x >> 2) & 0x22222222u));
 }
 
+// histogram (run-length SMEM atomics, as emit_tile) + counts / RGBA of one tile where
+// lane l holds pixels 32 l .. 32 l + 31: 8 x 16-B streaming stores of each per lane
+__device__ __forceinline__ void emit_direct(const uint32_t (&cnt32)[32], uint64_t tile, int lane,
+                                            const OverlapArgs &a, uint32_t *sh_hist,
+                                            const uint32_t *sh_lut, bool lut_sh) {
+  if (a.bins != nullptr) {
+    uint32_t cur = cnt32[0], run = 1;
+#pragma unroll
+    for (int j = 1; j < 32; ++j) {
+      const uint32_t c = cnt32[j];
+      if (c != cur) {
+        atomicAdd(sh_hist + cur, run);
+        cur = c;
+        run = 0;
+      }
+      ++run;
+    }
+    atomicAdd(sh_hist + cur, run);
+  }
+  const uint64_t px0 = (tile * 32 + (uint64_t)lane) * 32;
+  if (a.vec && px0 + 32 <= a.pixels) {
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const uint4 c = make_uint4(cnt32[4 * v], cnt32[4 * v + 1], cnt32[4 * v + 2], cnt32[4 * v + 3]);
+      if (a.counts) st_cs_v4(a.counts + px0 + 4 * v, c);
+      if (a.rgba) {
+        uint4 r;
+        if (lut_sh) {
+          r = make_uint4(sh_lut[c.x], sh_lut[c.y], sh_lut[c.z], sh_lut[c.w]);
+        } else {
+          r = make_uint4(rgba_word(c.x, a.n_inputs, a.lut), rgba_word(c.y, a.n_inputs, a.lut),
+                         rgba_word(c.z, a.n_inputs, a.lut), rgba_word(c.w, a.n_inputs, a.lut));
+        }
+        st_cs_v4(a.rgba + px0 + 4 * v, r);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (px0 + e < a.pixels) {
+        if (a.counts) a.counts[px0 + e] = cnt32[e];
+        if (a.rgba)
+          a.rgba[px0 + e] = lut_sh ? sh_lut[cnt32[e]] : rgba_word(cnt32[e], a.n_inputs, a.lut);
+      }
+  }
+}
+
 struct Args {
   const uint32_t *src;   // packed masks (tile-interleaved)
   uint64_t cap;          // slots per tile row of `src`
@@ -177,6 +229,8 @@ struct Args {
   int32_t *partial;      // one 256 x 256 int32 tile per CTA
 };
 
+// kSlots: the panel's masks are read through the slot table (a.slots != nullptr)
+template <bool kSlots>
 __global__ void __launch_bounds__(kThreads, 1)
     k_recompute_f4(const Args a, const OverlapArgs ov) {
   extern __shared__ uint8_t smem_raw[];
@@ -220,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t row = (uint32_t)(32 * gw + 4 * j) + ((uint32_t)lane >> 3);
 #ifndef FS_RC_NO_LOAD  // timing experiment only: no HBM traffic, constant data
       if (row < pk) {
-        const uint64_t slot = a.slots ? (uint64_t)sh_slot[row] : prow0 + row;
+        const uint64_t slot = kSlots ? (uint64_t)sh_slot[row] : prow0 + row;
         r[j] = ptx::ld_nc_v4(a.src + ((gu * a.cap + slot) * 32u + 4u * chunk));
       }
       else
@@ -239,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   // a contiguous run: first unit(s) in flight before the setup below (a slot list is
   // read into shared memory by the setup first)
-  if (is_exp && a.slots == nullptr) first_loads();
+  if (is_exp && !kSlots) first_loads();
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -254,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_mbar_init();
   }
   const bool lut_sh = ov.rgba != nullptr;
-  if (warp == kCntWarp0 && a.slots != nullptr) {  // this panel's slots and their span
+  if (kSlots && warp == kCntWarp0) {  // this panel's slots and their span
     uint32_t lo = 0xFFFFFFFFu, hi = 0u;
     for (uint32_t i = (uint32_t)lane; i < 256u; i += 32u) {
       const uint32_t sl = i < pk ? a.slots[256u * panel + i] : 0u;
@@ -287,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  if (is_exp && a.slots != nullptr) first_loads();
+  if (is_exp && kSlots) first_loads();
   const uint32_t tmem = *tmem_slot;
   if (warp >= 1 && warp <= 4) {  // every UE8M0 block scale = 1.0
     const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
@@ -417,8 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (gw == 0 && lane == 0 && u + FS_RC_L2PF < nunits) {
         // the unit's rows: a contiguous run, or the span of the slot list when it is
         // not much wider than the panel
-        const uint64_t lo = a.slots ? (uint64_t)sh_slot[256] : prow0;
-        const uint32_t n = a.slots ? sh_slot[257] - sh_slot[256] + 1u : pk;
+        const uint64_t lo = kSlots ? (uint64_t)sh_slot[256] : prow0;
+        const uint32_t n = kSlots ? sh_slot[257] - sh_slot[256] + 1u : pk;
         if (n <= 2u * pk)
           l2_prefetch(a.src + ((u0 + (uint64_t)(u + FS_RC_L2PF)) * a.cap + lo) * 32u, n * 128u);
       }
@@ -521,6 +575,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ov.partial16 != nullptr)  // several panels: this panel's counts, summed later
         emit_partial16(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb,
                        ov.partial16 + (uint64_t)panel * ov.part_pitch);
+      else if (FS_RC_DIRECT_EMIT)
+        emit_direct(cnt32, u0 + (uint64_t)u, lane, ov,
+                    sh_hist + (kHistCopies > 1 ? cw * kFuseBins : 0), sh_lut, lut_sh);
       else
         emit_tile<kHistMatch>(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov,
                               sh_hist + (kHistCopies > 1 ? cw * kFuseBins : 0),
@@ -554,10 +611,16 @@ cudaError_t launch_recompute_f4(const uint32_t *src, uint64_t cap, uint64_t row0
                                 uint32_t npanels, const uint32_t *slots) {
   if (kchunks == 0 || npanels == 0) return cudaSuccess;
   static SmemOptIn attr;
-  if (cudaError_t e = smem_opt_in(attr, rc::k_recompute_f4, (size_t)rc::kSmemBytes); e != cudaSuccess)
+  static SmemOptIn attr_slots;
+  if (cudaError_t e = slots ? smem_opt_in(attr_slots, rc::k_recompute_f4<true>, (size_t)rc::kSmemBytes)
+                            : smem_opt_in(attr, rc::k_recompute_f4<false>, (size_t)rc::kSmemBytes);
+      e != cudaSuccess)
     return e;
   rc::Args a{src, cap, row0, k, slots, total_units, upc, kchunks, partial};
-  rc::k_recompute_f4<<<kchunks * npanels, rc::kThreads, rc::kSmemBytes, s>>>(a, ov);
+  if (slots)
+    rc::k_recompute_f4<true><<<kchunks * npanels, rc::kThreads, rc::kSmemBytes, s>>>(a, ov);
+  else
+    rc::k_recompute_f4<false><<<kchunks * npanels, rc::kThreads, rc::kSmemBytes, s>>>(a, ov);
   return cudaGetLastError();
 }
 
