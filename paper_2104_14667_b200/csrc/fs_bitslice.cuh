@@ -136,27 +136,10 @@ constexpr int kTileTb = 36;  // transpose row stride (words): 16-B aligned, conf
 // bins (or global bins); padding pixels past a.pixels are counted in bin 0 and must be
 // removed once by the caller.  Counts / RGBA: transposed through `tb` and written with
 // 16-B streaming stores.
-// Histogram of one tile by warp aggregation: for pixel position j the 32 lanes hold 32
-// pixels' counts; __match_any_sync groups equal counts and one lane per group adds the
-// group size (distinct values per position, not pixels, become atomics).  Used where
-// neighbouring pixels rarely share a count (noisy ensembles defeat run-length merging).
-__device__ __forceinline__ void hist_tile_match(const uint32_t (&cnt32)[32], int lane,
-                                                uint32_t *sh_hist) {
-#pragma unroll 4
-  for (int j = 0; j < 32; ++j) {
-    const uint32_t c = cnt32[j];
-    const uint32_t m = __match_any_sync(0xFFFFFFFFu, c);
-    if ((m & ((1u << lane) - 1u)) == 0u) atomicAdd(sh_hist + c, (uint32_t)__popc(m));
-  }
-}
-
-template <bool kHistMatch = false>
 __device__ __forceinline__ void emit_tile(const uint32_t (&cnt32)[32], uint64_t tile, int lane,
                                           uint32_t *tb, const OverlapArgs &a, uint32_t *sh_hist,
                                           bool hist_sh, const uint32_t *sh_lut, bool lut_sh) {
-  if (kHistMatch && a.bins != nullptr && hist_sh) {
-    hist_tile_match(cnt32, lane, sh_hist);
-  } else if (a.bins != nullptr) {
+  if (a.bins != nullptr) {
     uint32_t cur = cnt32[0], run = 1;
 #pragma unroll
     for (int j = 1; j < 32; ++j) {

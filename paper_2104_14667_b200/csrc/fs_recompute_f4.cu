@@ -46,12 +46,6 @@ namespace rc {
 #define FS_RC_GROUPS 2
 #endif
 constexpr int kGroups = FS_RC_GROUPS;
-// histogram by warp-aggregated atomics (__match_any_sync per pixel position) instead of
-// per-lane run-length atomics
-#ifndef FS_RC_HIST_MATCH
-#define FS_RC_HIST_MATCH 0
-#endif
-constexpr bool kHistMatch = FS_RC_HIST_MATCH != 0;
 // every producing thread arrives on the stage / partial barriers itself (the arrive is the
 // release of that thread's own stores; 1) or one lane per warp after __syncwarp (0)
 #ifndef FS_RC_THREAD_ARRIVE
@@ -74,29 +68,18 @@ constexpr int kPlanes = 6;                    // bit planes of a 32-row partial 
 constexpr int kPartWords = 8 * kPlanes * 32;  // per unit (eight warps of one group)
 constexpr int kStageBytes = 256 * 128;        // 256 rows x 128 B (256 px of e2m1)
 constexpr int kFuseBins = 288;
-// one private SMEM histogram per combiner warp (1) or one shared by all of them (0)
-#ifndef FS_RC_PRIV_HIST
-#define FS_RC_PRIV_HIST 0
-#endif
-constexpr int kHistCopies = FS_RC_PRIV_HIST ? (FS_RC_GROUPS == 1 ? 4 : 3) : 1;  // = kCntWarps
 constexpr int kTbBytes = kCntWarps * 32 * kTileTb * 4;
-// emit counts / RGBA straight from each lane's 32 consecutive pixels (1) or through the
-// shared-memory transpose of emit_tile (0)
-#ifndef FS_RC_DIRECT_EMIT
-#define FS_RC_DIRECT_EMIT 0
-#endif
 constexpr int kSlotWords = 256 + 2;  // slot of every panel row + the slot span [lo, hi]
 constexpr int kExtraBytes = kPartDepth * kPartWords * 4 + kTbBytes +
-                            (kHistCopies + 1) * kFuseBins * 4 + kSlotWords * 4;
+                            2 * kFuseBins * 4 + kSlotWords * 4;
 constexpr int kSmemMax = 232448;
 constexpr int kStages = (kSmemMax - 1024 - 512 - kExtraBytes) / kStageBytes;
 constexpr int kSmemBytes = kStages * kStageBytes + kExtraBytes + 1024 + 512;
 static_assert(kStages >= 3, "operand ring too shallow");
+// operand stages written per proxy fence + arrive (2 measured better with one expander
+// group, 1 with two)
 #ifndef FS_RC_BATCH
 #define FS_RC_BATCH 1
-#endif
-#ifndef FS_RC_COUNT_MID
-#define FS_RC_COUNT_MID 0
 #endif
 // L2 prefetch distance in units: while unit u is processed, one lane bulk-prefetches unit
 // u + d (cp.async.bulk.prefetch.L2, the unit's k rows x 128 B are contiguous) so the
@@ -104,12 +87,7 @@ static_assert(kStages >= 3, "operand ring too shallow");
 #ifndef FS_RC_L2PF
 #define FS_RC_L2PF 4
 #endif
-// L2 policy of the prefetched units: 1 = evict_last, 0 = default
-#ifndef FS_RC_PF_HINT
-#define FS_RC_PF_HINT 0
-#endif
 constexpr int kBatch = FS_RC_BATCH;             // operand stages per proxy fence
-constexpr bool kCountMid = FS_RC_COUNT_MID != 0;  // count between the two stage halves
 static_assert(4 % kBatch == 0 && kBatch < kStages, "batch must divide a unit's 4 stages");
 __host__ __device__ constexpr int part_slot(int u) {
   return (u % kGroups) * kPartSlots + (u / kGroups) % kPartSlots;
@@ -118,15 +96,7 @@ __host__ __device__ constexpr int part_use(int u) { return (u / kGroups) / kPart
 
 // bulk L2 prefetch of one unit (k rows x 128 B, contiguous)
 __device__ __forceinline__ void l2_prefetch(const void *p, uint32_t bytes) {
-#if FS_RC_PF_HINT
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes),
-               "l"(pol)
-               : "memory");
-#else
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-#endif
 }
 
 // (h, l) = a + b (half adder)
@@ -169,53 +139,6 @@ __device__ __forceinline__ void expand_word(uint32_t addr, uint32_t x) {
                                     (x >> 1) & 0x22222222u, (x >> 2) & 0x22222222u));
 }
 
-// histogram (run-length SMEM atomics, as emit_tile) + counts / RGBA of one tile where
-// lane l holds pixels 32 l .. 32 l + 31: 8 x 16-B streaming stores of each per lane
-__device__ __forceinline__ void emit_direct(const uint32_t (&cnt32)[32], uint64_t tile, int lane,
-                                            const OverlapArgs &a, uint32_t *sh_hist,
-                                            const uint32_t *sh_lut, bool lut_sh) {
-  if (a.bins != nullptr) {
-    uint32_t cur = cnt32[0], run = 1;
-#pragma unroll
-    for (int j = 1; j < 32; ++j) {
-      const uint32_t c = cnt32[j];
-      if (c != cur) {
-        atomicAdd(sh_hist + cur, run);
-        cur = c;
-        run = 0;
-      }
-      ++run;
-    }
-    atomicAdd(sh_hist + cur, run);
-  }
-  const uint64_t px0 = (tile * 32 + (uint64_t)lane) * 32;
-  if (a.vec && px0 + 32 <= a.pixels) {
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const uint4 c = make_uint4(cnt32[4 * v], cnt32[4 * v + 1], cnt32[4 * v + 2], cnt32[4 * v + 3]);
-      if (a.counts) st_cs_v4(a.counts + px0 + 4 * v, c);
-      if (a.rgba) {
-        uint4 r;
-        if (lut_sh) {
-          r = make_uint4(sh_lut[c.x], sh_lut[c.y], sh_lut[c.z], sh_lut[c.w]);
-        } else {
-          r = make_uint4(rgba_word(c.x, a.n_inputs, a.lut), rgba_word(c.y, a.n_inputs, a.lut),
-                         rgba_word(c.z, a.n_inputs, a.lut), rgba_word(c.w, a.n_inputs, a.lut));
-        }
-        st_cs_v4(a.rgba + px0 + 4 * v, r);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < 32; ++e)
-      if (px0 + e < a.pixels) {
-        if (a.counts) a.counts[px0 + e] = cnt32[e];
-        if (a.rgba)
-          a.rgba[px0 + e] = lut_sh ? sh_lut[cnt32[e]] : rgba_word(cnt32[e], a.n_inputs, a.lut);
-      }
-  }
-}
-
 struct Args {
   const uint32_t *src;   // packed masks (tile-interleaved)
   uint64_t cap;          // slots per tile row of `src`
@@ -241,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *part = reinterpret_cast<uint32_t *>(smem + kStages * kStageBytes);
   uint32_t *cnt_tb = part + kPartDepth * kPartWords;
   uint32_t *sh_hist = cnt_tb + kCntWarps * 32 * kTileTb;
-  uint32_t *sh_lut = sh_hist + kHistCopies * kFuseBins;
+  uint32_t *sh_lut = sh_hist + kFuseBins;
   uint32_t *sh_slot = sh_lut + kFuseBins;  // ensemble slot of panel row r; [256], [257]: span
   uint64_t *full = reinterpret_cast<uint64_t *>(sh_slot + kSlotWords);
   uint64_t *empty = full + kStages;
@@ -327,8 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp >= kCntWarp0) {
     for (int i = tid - 32 * kCntWarp0; i < kFuseBins; i += 32 * kCntWarps) {
-#pragma unroll
-      for (int c = 0; c < kHistCopies; ++c) sh_hist[c * kFuseBins + i] = 0;
+      sh_hist[i] = 0;
       sh_lut[i] = lut_sh && (uint32_t)i < ov.nbins ? rgba_word(i, ov.n_inputs, ov.lut) : 0u;
     }
   }
@@ -477,11 +399,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           l2_prefetch(a.src + ((u0 + (uint64_t)(u + FS_RC_L2PF)) * a.cap + lo) * 32u, n * 128u);
       }
 #endif
-      if (!kCountMid) count_unit(u, r);
+      count_unit(u, r);
 #pragma unroll
       for (int s0 = 0; s0 < 4; s0 += kBatch) {
         stage_batch(u, r, s0);
-        if (kCountMid && s0 + kBatch == 2) count_unit(u, r);
       }
     };
     if (kGroups == 1) {
@@ -575,23 +496,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ov.partial16 != nullptr)  // several panels: this panel's counts, summed later
         emit_partial16(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb,
                        ov.partial16 + (uint64_t)panel * ov.part_pitch);
-      else if (FS_RC_DIRECT_EMIT)
-        emit_direct(cnt32, u0 + (uint64_t)u, lane, ov,
-                    sh_hist + (kHistCopies > 1 ? cw * kFuseBins : 0), sh_lut, lut_sh);
       else
-        emit_tile<kHistMatch>(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov,
-                              sh_hist + (kHistCopies > 1 ? cw * kFuseBins : 0),
-                              ov.bins != nullptr, sh_lut, lut_sh);
+        emit_tile(cnt32, u0 + (uint64_t)u, lane, cnt_tb + cw * 32 * kTileTb, ov, sh_hist,
+                  ov.bins != nullptr, sh_lut, lut_sh);
     }
   }
   __syncthreads();
   if (warp >= kCntWarp0 && ov.bins != nullptr) {
-    for (uint32_t i = tid - 32 * kCntWarp0; i < ov.nbins; i += 32 * kCntWarps) {
-      uint32_t h = 0;
-#pragma unroll
-      for (int c = 0; c < kHistCopies; ++c) h += sh_hist[c * kFuseBins + i];
-      if (h) atomicAdd(ov.bins + i, (unsigned long long)h);
-    }
+    for (uint32_t i = tid - 32 * kCntWarp0; i < ov.nbins; i += 32 * kCntWarps)
+      if (sh_hist[i]) atomicAdd(ov.bins + i, (unsigned long long)sh_hist[i]);
     if (blockIdx.x == 0 && tid == 32 * kCntWarp0) {
       const uint64_t padpx = a.total_units * 1024 - ov.pixels;  // padding counted in bin 0
       if (padpx) atomicAdd(ov.bins, (unsigned long long)(0ull - padpx));
