@@ -843,7 +843,9 @@ def main():
     if world == 1 or backend == "nccl":
         # the C++ frame loop; with N ranks each runs its band and the per-frame exchange is
         # an ncclAllReduce inside the loop (fs_comm, ShardedEnsemble.pipeline).  A failure
-        # here is reported in the line instead of aborting the measured numbers above.
+        # is reported in the line instead of aborting the measured numbers above; every
+        # rank learns whether any rank failed before the max-over-ranks collectives.
+        err, dev_ms, wall_n, ncl = None, 0.0, 0.0, 0
         try:
             mk = (ens.pipeline(slots, tau=args.tau, engine=args.engine, ids=ids, depth=depth)
                   if world == 1 else
@@ -851,20 +853,23 @@ def main():
             with mk as pipe:
                 pipe.run(args.warmup)
                 torch.cuda.synchronize()
-                barrier()
                 t0n = time.perf_counter()
                 rn = pipe.run(rsteps)
                 wall_n = time.perf_counter() - t0n
-            native = {"ms_per_step": round(max_over_ranks(rn["device_ms"]) / rsteps, 4),
-                      "fps": round(rsteps / (max_over_ranks(rn["device_ms"]) / 1e3), 3),
+            dev_ms, ncl = rn["device_ms"], len(rn["clusters"])
+        except Exception as exc:  # noqa: BLE001
+            err = f"{type(exc).__name__}: {str(exc)[:300]}"
+        if int(max_over_ranks(1.0 if err else 0.0)):
+            native = {"error": err or "failed on another rank"}
+        else:
+            native = {"ms_per_step": round(max_over_ranks(dev_ms) / rsteps, 4),
+                      "fps": round(rsteps / (max_over_ranks(dev_ms) / 1e3), 3),
                       "wall_ms_per_step": round(max_over_ranks(wall_n) / rsteps * 1e3, 4),
-                      "clusters": len(rn["clusters"]),
+                      "clusters": ncl,
                       "path": "fs_pipeline_run: recompute + device Jaccard/outliers + D2H queued "
                               "while C++ workers run the linkage (no Python per frame)"
                               + ("" if world == 1 else "; per-frame ncclAllReduce of "
                                  "[bins | Gram] inside the C++ loop (fs_comm)")}
-        except Exception as exc:  # noqa: BLE001
-            native = {"error": f"{type(exc).__name__}: {str(exc)[:300]}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and host is not None:

@@ -85,13 +85,23 @@ class NativeComm:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         uid = (C.c_uint8 * 128)()
+        err = None
         if self.rank == 0:
-            N.call("fs_comm_unique_id", uid)
+            try:
+                N.call("fs_comm_unique_id", uid)
+            except (RuntimeError, ValueError) as exc:
+                err = str(exc)
         if self.world > 1:
-            obj = [bytes(uid)]
+            # every rank learns rank 0's outcome, so a failure cannot leave the others
+            # waiting inside the collective init
+            obj = [None if err else bytes(uid)]
             dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0)
                                        if group is not None else 0, group=group)
+            if obj[0] is None:
+                raise RuntimeError(f"fs_comm_unique_id failed on rank 0: {err or '?'}")
             uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        elif err:
+            raise RuntimeError(err)
         dev = torch.cuda.current_device() if device is None else int(device)
         N.set_device(dev)
         h = C.c_void_p()
