@@ -936,6 +936,8 @@ size_t gram_tc_gather_bytes(uint32_t k, uint64_t wpm) { return (size_t)k * wpm *
 // Fused single-panel FP4 recompute: 2 = k_recompute_f4 (register-staged raw units,
 // fs_recompute_f4.cu, default), 1 = k_gram_tc<256, ..., FUSE> (TMA raw ring + counter
 // warps).  FS_FUSED_KERNEL=1 selects the older kernel (A/B measurements).
+constexpr uint32_t kRc128MinMasks = 80;
+
 static int fused_kernel_version() {
   static const int v = [] {
     const char *e = std::getenv("FS_FUSED_KERNEL");
@@ -959,8 +961,8 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
   const int64_t first = contiguous_run(host_slots, k);
   cudaError_t e;
   // the single-panel fused recompute reads scattered slots itself (no gather pass)
-  const bool rc_direct = fuse != nullptr && p.npanels == 1 && fp4 && p.panel == 256 &&
-                         fused_kernel_version() >= 2;
+  const bool rc_direct = fuse != nullptr && p.npanels == 1 && fp4 &&
+                         (p.panel == 256 || k >= kRc128MinMasks) && fused_kernel_version() >= 2;
   if (first >= 0) {
     row0 = (uint64_t)first;
   } else if (rc_direct) {
@@ -1011,7 +1013,13 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
     ovp.part_pitch = pitch;
   }
   if (p.panel == 128) {
-    if (fuse_now)
+    // 128-row k_recompute_f4 from k = 80 on; below it the narrow TMA-ring kernel's MMA
+    // N shrinks with k and its per-unit overhead is lower (k_sweep: k = 64 0.57 vs 0.58 ms,
+    // k = 100 0.60 vs 0.58, k = 128 0.67 vs 0.58; profiles/round2/kernel_search/g36)
+    if (fuse_now && fp4 && k >= kRc128MinMasks && fused_kernel_version() >= 2)
+      e = launch_recompute_f4(src, src_cap, row0, k, p.units_diag, p.kc_diag, p.upc_diag,
+                              part_diag, *fuse, s, 1, first >= 0 ? nullptr : slots, 128);
+    else if (fuse_now)
       e = fp4 ? launch_one<128, true, true, true>(tm_diag, p, part_diag, *fuse, s)
               : launch_one<128, true, false, true>(tm_diag, p, part_diag, *fuse, s);
     else

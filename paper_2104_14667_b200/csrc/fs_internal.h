@@ -121,11 +121,13 @@ cudaError_t launch_gram_tc(const uint32_t *packed, uint64_t capacity, uint64_t w
 // (blockIdx = panel * kchunks + chunk); with ov.partial16 set each panel's counts go to
 // its uint16 slab (ov.part_pitch apart) for launch_combine_partials.
 // slots != nullptr (device list, npanels == 1): mask m is read from slot slots[m] of the
-// ensemble directly, with no gather pass.
+// ensemble directly, with no gather pass.  rows = 128: a single panel of k <= 128 masks
+// (one MMA of N = roundup(k, 16) per K step, 128 x 128 partial tiles for k_gram_reduce<128>).
 cudaError_t launch_recompute_f4(const uint32_t *src, uint64_t cap, uint64_t row0, uint32_t k,
                                 uint64_t total_units, uint32_t kchunks, uint64_t upc,
                                 int32_t *partial, const OverlapArgs &ov, cudaStream_t s,
-                                uint32_t npanels = 1, const uint32_t *slots = nullptr);
+                                uint32_t npanels = 1, const uint32_t *slots = nullptr,
+                                uint32_t rows = 256);
 // fuse != nullptr: when all k masks fit one panel (k <= 256) the diagonal CTAs also
 // run the overlap pass (counts / histogram / RGBA of `*fuse`, weights 1) and *fused is
 // set; bins must be zeroed by the caller.  Otherwise nothing of *fuse is written.

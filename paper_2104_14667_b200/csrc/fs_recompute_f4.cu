@@ -54,28 +54,36 @@ constexpr int kGroups = FS_RC_GROUPS;
 constexpr bool kThreadArrive = FS_RC_THREAD_ARRIVE != 0;
 constexpr uint32_t kArrivePerWarp = kThreadArrive ? 32u : 1u;
 static_assert(kGroups == 1 || kGroups == 2, "one or two expander groups");
-constexpr int kExpWarps = 8 * kGroups;        // expander / epilogue warps (8 per group)
 constexpr int kCntWarps = kGroups == 1 ? 4 : 3;  // combiner + emit warps
-constexpr int kWarps = 1 + kExpWarps + kCntWarps;
-constexpr int kThreads = 32 * kWarps;
-constexpr int kCntWarp0 = 1 + kExpWarps;
 // partial-count ring: kCntWarps slots per group; combiner c owns slot c of every group's
 // ring and takes the units u with (u / kGroups) % kCntWarps == c, in order — one producer
 // group and one consumer per slot, so the parity waits cannot alias
 constexpr int kPartSlots = kCntWarps;
 constexpr int kPartDepth = kGroups * kPartSlots;
 constexpr int kPlanes = 6;                    // bit planes of a 32-row partial count
-constexpr int kPartWords = 8 * kPlanes * 32;  // per unit (eight warps of one group)
-constexpr int kStageBytes = 256 * 128;        // 256 rows x 128 B (256 px of e2m1)
 constexpr int kFuseBins = 288;
 constexpr int kTbBytes = kCntWarps * 32 * kTileTb * 4;
 constexpr int kSlotWords = 256 + 2;  // slot of every panel row + the slot span [lo, hi]
-constexpr int kExtraBytes = kPartDepth * kPartWords * 4 + kTbBytes +
-                            2 * kFuseBins * 4 + kSlotWords * 4;
 constexpr int kSmemMax = 232448;
-constexpr int kStages = (kSmemMax - 1024 - 512 - kExtraBytes) / kStageBytes;
-constexpr int kSmemBytes = kStages * kStageBytes + kExtraBytes + 1024 + 512;
-static_assert(kStages >= 3, "operand ring too shallow");
+
+// ROWS = 256: a 256-mask panel, MMAs rows 0-127 x N=256 + rows 128-255 x N=128 per K step;
+// ROWS = 128: a panel of k <= 128 masks, one MMA rows 0-127 x N=roundup(k, 16).
+template <int ROWS>
+struct Cfg {
+  static constexpr int kGW = ROWS / 32;                 // expander warps per group
+  static constexpr int kExpWarps = kGW * kGroups;       // expander / epilogue warps
+  static constexpr int kWarps = 1 + kExpWarps + kCntWarps;
+  static constexpr int kThreads = 32 * kWarps;
+  static constexpr int kCntWarp0 = 1 + kExpWarps;
+  static constexpr int kPartWords = kGW * kPlanes * 32;  // per unit
+  static constexpr int kStageBytes = ROWS * 128;        // ROWS rows x 128 B (256 px of e2m1)
+  static constexpr int kExtraBytes = kPartDepth * kPartWords * 4 + kTbBytes +
+                                     2 * kFuseBins * 4 + kSlotWords * 4;
+  static constexpr int kStages = (kSmemMax - 1024 - 512 - kExtraBytes) / kStageBytes;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kExtraBytes + 1024 + 512;
+  static_assert(kStages >= 3, "operand ring too shallow");
+  static_assert(2 * (2 * kStages + 2 * kPartDepth + 1) * 4 + 12 <= 512, "barrier area");
+};
 // operand stages written per proxy fence + arrive (2 measured better with one expander
 // group, 1 with two)
 #ifndef FS_RC_BATCH
@@ -88,7 +96,7 @@ static_assert(kStages >= 3, "operand ring too shallow");
 #define FS_RC_L2PF 4
 #endif
 constexpr int kBatch = FS_RC_BATCH;             // operand stages per proxy fence
-static_assert(4 % kBatch == 0 && kBatch < kStages, "batch must divide a unit's 4 stages");
+static_assert(4 % kBatch == 0 && kBatch < 3, "batch must divide a unit's 4 stages");
 __host__ __device__ constexpr int part_slot(int u) {
   return (u % kGroups) * kPartSlots + (u / kGroups) % kPartSlots;
 }
@@ -149,13 +157,16 @@ struct Args {
   uint64_t total_units;  // tiles of 1024 px
   uint64_t upc;          // units per CTA chunk
   uint32_t kchunks;      // CTA chunks per panel: blockIdx.x = panel * kchunks + chunk
-  int32_t *partial;      // one 256 x 256 int32 tile per CTA
+  int32_t *partial;      // one ROWS x ROWS int32 tile per CTA
 };
 
 // kSlots: the panel's masks are read through the slot table (a.slots != nullptr)
-template <bool kSlots>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int ROWS, bool kSlots>
+__global__ void __launch_bounds__(Cfg<ROWS>::kThreads, 1)
     k_recompute_f4(const Args a, const OverlapArgs ov) {
+  using C = Cfg<ROWS>;
+  constexpr int kGW = C::kGW, kExpWarps = C::kExpWarps, kCntWarp0 = C::kCntWarp0;
+  constexpr int kPartWords = C::kPartWords, kStageBytes = C::kStageBytes, kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   const uint32_t pad = (1024u - (raw_addr & 1023u)) & 1023u;
@@ -178,8 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // diagonal tile `panel` of a k > 256 ensemble (the Gram of masks 256 panel ..) or the
   // single panel (panel 0); the off-diagonal tiles run on k_gram_pair_f4
   const uint32_t panel = blockIdx.x / a.kchunks;
-  const uint64_t prow0 = a.row0 + 256ull * panel;            // first slot of this panel
-  const uint32_t pk = min(256u, a.k - 256u * panel);         // masks in this panel
+  const uint64_t prow0 = a.row0 + (uint64_t)ROWS * panel;     // first slot of this panel
+  const uint32_t pk = min((uint32_t)ROWS, a.k - (uint32_t)ROWS * panel);  // masks in it
   const uint64_t u0 = (uint64_t)(blockIdx.x % a.kchunks) * a.upc;
   const uint64_t u1 = min(u0 + a.upc, a.total_units);
   const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
@@ -187,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // expander registers: rows 4j + lane/8 of this warp's 32 rows, chunk lane % 8
   const int ew = warp - 1;
-  const int grp = ew / 8, gw = ew % 8;  // expander group, warp within the group
+  const int grp = ew / kGW, gw = ew % kGW;  // expander group, warp within the group
   const uint32_t chunk = (uint32_t)lane & 7u;
   uint4 ra[8], rb[8];
   auto load_unit = [&](int u, uint4 (&r)[8]) {
@@ -220,11 +231,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], 8 * kArrivePerWarp);  // the eight warps of the unit's group
+      ptx::mbar_init(&full[s], kGW * kArrivePerWarp);  // the warps of the unit's group
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kPartDepth; ++s) {
-      ptx::mbar_init(&part_full[s], 8 * kArrivePerWarp);
+      ptx::mbar_init(&part_full[s], kGW * kArrivePerWarp);
       ptx::mbar_init(&part_empty[s], kArrivePerWarp);
     }
     ptx::mbar_init(tmem_full, 1);
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (kSlots && warp == kCntWarp0) {  // this panel's slots and their span
     uint32_t lo = 0xFFFFFFFFu, hi = 0u;
     for (uint32_t i = (uint32_t)lane; i < 256u; i += 32u) {
-      const uint32_t sl = i < pk ? a.slots[256u * panel + i] : 0u;
+      const uint32_t sl = i < pk ? a.slots[(uint32_t)ROWS * panel + i] : 0u;
       sh_slot[i] = sl;
       if (i < pk) {
         lo = min(lo, sl);
@@ -280,6 +291,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0 && nst > 0) {
       constexpr uint32_t idA = tc::idesc_mxf4(128, 256);
       constexpr uint32_t idB = tc::idesc_mxf4(128, 128);
+      // ROWS = 128: N = roundup(k, 16) columns (rows >= k are zeros and unread)
+      const uint32_t idN = tc::idesc_mxf4(128, (int)min(128u, (pk + 15u) & ~15u));
       const uint32_t sfa = tmem + tc::kSfCol, sfb = tmem + tc::kSfCol + 16;
       const uint64_t d_op = tc::sw128_desc(op_base);
       for (int j = 0; j < nst; ++j) {
@@ -293,8 +306,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t lo = d_s + (uint64_t)((ks * 32) >> 4);
           const uint64_t hi = lo + (uint64_t)((128 * 128) >> 4);
 #ifndef FS_RC_NO_MMA  // timing experiment only
-          tc::mma_mxf4(tmem, lo, lo, idA, acc, sfa, sfb);          // rows 0-127 x 0-255
-          tc::mma_mxf4(tmem + 256u, hi, hi, idB, acc, sfa, sfb);   // rows 128-255 x 128-255
+          if (ROWS == 256) {
+            tc::mma_mxf4(tmem, lo, lo, idA, acc, sfa, sfb);          // rows 0-127 x 0-255
+            tc::mma_mxf4(tmem + 256u, hi, hi, idB, acc, sfa, sfb);   // rows 128-255 x 128-255
+          } else {
+            tc::mma_mxf4(tmem, lo, lo, idN, acc, sfa, sfb);          // rows 0-127 x 0-(N-1)
+          }
+#else
+          (void)hi;
+          (void)idN;
 #endif
         }
         tc::mma_commit(&empty[s]);
@@ -424,17 +444,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // ===== epilogue: TMEM -> registers -> int32 partial tile =====
     const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter of this warp
-    const int cg = gw / 4;                    // two warps per quarter split the columns
-    int32_t *out = a.partial + (uint64_t)blockIdx.x * 256 * 256;
+    const int cg = gw / 4;                    // warps sharing a quarter split the columns
+    constexpr int kColStep = 32 * (kGW / 4);
+    int32_t *out = a.partial + (uint64_t)blockIdx.x * ROWS * ROWS;
     if (grp == 0 && nst > 0) {
       ptx::mbar_wait(tmem_full, 0);
       tc::fence_after();
     }
 #pragma unroll
-    for (int h = 0; h < 2 && grp == 0; ++h) {  // group 0 drains the accumulators
+    for (int h = 0; h < ROWS / 128 && grp == 0; ++h) {  // group 0 drains the accumulators
       const uint32_t row = h * 128 + q * 32 + lane;
       const int c_begin = h == 1 ? 128 : 0;
-      for (int c0 = c_begin + 32 * cg; c0 < 256; c0 += 64) {
+      for (int c0 = c_begin + 32 * cg; c0 < ROWS; c0 += kColStep) {
         uint32_t v[32];
         const uint32_t col = h == 1 ? (256u + (uint32_t)(c0 - 128)) : (uint32_t)c0;
         tc::tmem_ld32(tmem + ((q * 32u) << 16) + col, v);
@@ -445,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = (uint32_t)__float2int_rn(__uint_as_float(v[e]));
         }
-        int4 *dst = reinterpret_cast<int4 *>(out + (uint64_t)row * 256 + c0);
+        int4 *dst = reinterpret_cast<int4 *>(out + (uint64_t)row * ROWS + c0);
 #pragma unroll
         for (int e = 0; e < 8; ++e)
           dst[e] = make_int4((int)v[4 * e], (int)v[4 * e + 1], (int)v[4 * e + 2], (int)v[4 * e + 3]);
@@ -463,9 +484,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ps = part_slot(u);
       ptx::mbar_wait(&part_full[ps], (uint32_t)(part_use(u) & 1));
       const uint32_t *src = part + ps * kPartWords + lane;
-      uint32_t n[8][kPlanes];
+      uint32_t n[kGW][kPlanes];
 #pragma unroll
-      for (int w = 0; w < 8; ++w)
+      for (int w = 0; w < kGW; ++w)
 #pragma unroll
         for (int p = 0; p < kPlanes; ++p) n[w][p] = src[(w * kPlanes + p) * 32];
       if (kThreadArrive) {
@@ -474,21 +495,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&part_empty[ps]);
       }
-      uint32_t s7[4][7], s8[2][8], s9[9];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) add_planes<6>(n[2 * i], n[2 * i + 1], s7[i]);
-#pragma unroll
-      for (int i = 0; i < 2; ++i) add_planes<7>(s7[2 * i], s7[2 * i + 1], s8[i]);
-      add_planes<8>(s8[0], s8[1], s9);
-      HSCounter<5> hc;
-      hc.ones = s9[0];
-      hc.twos = s9[1];
-      hc.fours = s9[2];
-      hc.eights = s9[3];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) hc.H[i] = s9[4 + i];
       uint32_t cnt32[32];
-      hc.extract1(cnt32);
+      if constexpr (kGW == 8) {  // 8 x 32 rows -> 9 planes
+        uint32_t s7[4][7], s8[2][8], s9[9];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) add_planes<6>(n[2 * i], n[2 * i + 1], s7[i]);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) add_planes<7>(s7[2 * i], s7[2 * i + 1], s8[i]);
+        add_planes<8>(s8[0], s8[1], s9);
+        HSCounter<5> hc;
+        hc.ones = s9[0];
+        hc.twos = s9[1];
+        hc.fours = s9[2];
+        hc.eights = s9[3];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) hc.H[i] = s9[4 + i];
+        hc.extract1(cnt32);
+      } else {  // 4 x 32 rows -> 8 planes
+        uint32_t s7[2][7], s8[8];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) add_planes<6>(n[2 * i], n[2 * i + 1], s7[i]);
+        add_planes<7>(s7[0], s7[1], s8);
+        HSCounter<4> hc;
+        hc.ones = s8[0];
+        hc.twos = s8[1];
+        hc.fours = s8[2];
+        hc.eights = s8[3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hc.H[i] = s8[4 + i];
+        hc.extract1(cnt32);
+      }
 #ifdef FS_RC_NO_EMIT  // timing experiment only
       if (cnt32[lane & 31] == 0xFFFFFFFFu) ov.counts[0] = 0;  // keep the count live
       continue;
@@ -518,23 +554,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace rc
 
+namespace {
+template <int ROWS, bool SLOTS>
+cudaError_t launch_rc(const rc::Args &a, const OverlapArgs &ov, unsigned grid, cudaStream_t s) {
+  using C = rc::Cfg<ROWS>;
+  static SmemOptIn attr;
+  if (cudaError_t e = smem_opt_in(attr, rc::k_recompute_f4<ROWS, SLOTS>, (size_t)C::kSmemBytes);
+      e != cudaSuccess)
+    return e;
+  rc::k_recompute_f4<ROWS, SLOTS><<<grid, C::kThreads, C::kSmemBytes, s>>>(a, ov);
+  return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_recompute_f4(const uint32_t *src, uint64_t cap, uint64_t row0, uint32_t k,
                                 uint64_t total_units, uint32_t kchunks, uint64_t upc,
                                 int32_t *partial, const OverlapArgs &ov, cudaStream_t s,
-                                uint32_t npanels, const uint32_t *slots) {
+                                uint32_t npanels, const uint32_t *slots, uint32_t rows) {
   if (kchunks == 0 || npanels == 0) return cudaSuccess;
-  static SmemOptIn attr;
-  static SmemOptIn attr_slots;
-  if (cudaError_t e = slots ? smem_opt_in(attr_slots, rc::k_recompute_f4<true>, (size_t)rc::kSmemBytes)
-                            : smem_opt_in(attr, rc::k_recompute_f4<false>, (size_t)rc::kSmemBytes);
-      e != cudaSuccess)
-    return e;
+  if (rows != 128 && rows != 256) return cudaErrorInvalidValue;
   rc::Args a{src, cap, row0, k, slots, total_units, upc, kchunks, partial};
-  if (slots)
-    rc::k_recompute_f4<true><<<kchunks * npanels, rc::kThreads, rc::kSmemBytes, s>>>(a, ov);
-  else
-    rc::k_recompute_f4<false><<<kchunks * npanels, rc::kThreads, rc::kSmemBytes, s>>>(a, ov);
-  return cudaGetLastError();
+  const unsigned grid = kchunks * npanels;
+  if (rows == 256)
+    return slots ? launch_rc<256, true>(a, ov, grid, s) : launch_rc<256, false>(a, ov, grid, s);
+  return slots ? launch_rc<128, true>(a, ov, grid, s) : launch_rc<128, false>(a, ov, grid, s);
 }
 
 }  // namespace fs
