@@ -6,6 +6,9 @@
 // _kernels_np.py:26-32) and accumulate / overlap_histogram / composite_map
 // (analytics.py:106-162, _kernels_np.py:16-47) of /root/reference/pkg/src/floodstream/.
 //
+// Template ROWS: 256 (one 256-mask panel, also the diagonal tiles of larger ensembles) or
+// 128 (a single panel of 80..128 masks, one MMA of N = roundup(k, 16) per K step).
+//
 // Data path per 1024-px unit (one pixel tile of every mask = 256 x 128 B, contiguous in
 // the tile-interleaved layout, fs_common.cuh):
 //   * Two groups of 8 expander warps take alternate units (FS_RC_GROUPS = 2; group g
