@@ -96,7 +96,7 @@ struct Cfg {
 // u + d (cp.async.bulk.prefetch.L2, the unit's k rows x 128 B are contiguous) so the
 // register loads issued two units ahead hit L2 (0 = off)
 #ifndef FS_RC_L2PF
-#define FS_RC_L2PF 4
+#define FS_RC_L2PF 2
 #endif
 constexpr int kBatch = FS_RC_BATCH;             // operand stages per proxy fence
 static_assert(4 % kBatch == 0 && kBatch < 3, "batch must divide a unit's 4 stages");
