@@ -17,7 +17,7 @@
 //     from global memory into REGISTERS with fully coalesced 16-B loads (warp
 //     instruction j covers 4 consecutive mask rows = 512 contiguous bytes); lane l holds
 //     rows 4j + l/8 (j = 0..7), 16-B chunk c = l % 8 (pixels 128c .. 128c+127).  One lane
-//     per group bulk-prefetches the unit 4 ahead into L2 (cp.async.bulk.prefetch.L2), so
+//     per group bulk-prefetches the unit 2 ahead into L2 (cp.async.bulk.prefetch.L2), so
 //     the register loads, issued as soon as the previous unit is expanded, hit L2.  No
 //     TMA ring and no raw copy in shared memory.
 //   * Counting from those registers: per lane a carry-save tree over its 8 rows, then
